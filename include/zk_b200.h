@@ -1,0 +1,155 @@
+/*
+ * zk_b200.h -- C ABI of the B200-native Zernike radial-basis library
+ * (libzk_b200.so). Plain pointers and sizes; no torch or CUDA types.
+ *
+ * The reference (zernkit, a pure-Python package, /root/reference/pkg/src/
+ * zernkit = "zk/") has no FFI: its boundary for this path is five Python
+ * functions. Each entry point below names the reference interface it
+ * replaces; the Python host mirror (paper_2409_19156_b200/) binds these with
+ * ctypes and keeps the reference's names, argument meaning and exceptions.
+ *
+ *   zk_plan_create / zk_plan_describe   <- zk/modes.py:108-125 dedup_plan
+ *                                          + zk/batch.py:61-66 _alpha_groups
+ *   zk_step_counters                    <- zk/batch.py:69-94 cached_step_counter /
+ *                                          independent_step_counter
+ *   zk_radial_eval                      <- zk/batch.py:104-142 batch_cached,
+ *                                          zk/batch.py:145-181 batch_independent,
+ *                                          zk/batch.py:184-190 evaluate_batch,
+ *                                          zk/evaluate.py:157-186 radial_jacobi
+ *                                          (jacobi_chain :36-76 + assemble_radial
+ *                                          :102-154 fused; scatter :97-101 fused)
+ *   zk_zernike_eval                     <- zk/evaluate.py:259-274 zernike_eval
+ *                                          (radial x cos/sin, all columns at once)
+ *   zk_series_eval                      <- new (B @ c; oracle numpy)
+ *   zk_gram_accumulate                  <- new (B^T B, B^T y; nearest
+ *                                          reference: tests/test_acceptance.py:150-172)
+ *
+ * Conventions
+ *   - Every function returns int: ZK_OK (0) or a negative ZK_E* code; the
+ *     message of the last failure on the calling thread is zk_last_error().
+ *   - Matrices are column-major ("point-fastest", the reference's F-order
+ *     EvalMatrix layout, zk/batch.py:98): element (p, col) at out[col*ld + p].
+ *   - Modes are (n, m) int32 pairs, m signed; validity is the reference's
+ *     Mode invariant (zk/modes.py:37-43). Invalid modes -> ZK_EINVAL.
+ *   - Memory: pointers are device pointers unless the ZK_HOST_* flag for
+ *     that argument is set. Host outputs are written through a chunked,
+ *     double-buffered device->host pipeline. Caller owns every buffer.
+ *   - Reentrant: state lives in zk_ctx (one CUDA stream + scratch per ctx).
+ *     Distinct contexts may be used from distinct threads concurrently.
+ *   - There is no CPU fallback: without a usable CUDA device every compute
+ *     entry point fails with ZK_ENODEV / ZK_ECUDA.
+ */
+#ifndef ZK_B200_H
+#define ZK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZK_OK        0
+#define ZK_EINVAL   -1   /* bad argument (mode, size, order, pointer) */
+#define ZK_ECUDA    -2   /* CUDA runtime error */
+#define ZK_ENOMEM   -3   /* allocation failed */
+#define ZK_ENODEV   -4   /* no CUDA device */
+
+/* flags */
+#define ZK_HOST_INPUT   1u   /* rho / theta / coef / y are host pointers      */
+#define ZK_HOST_OUTPUT  2u   /* out / f / G / Bty are host pointers           */
+#define ZK_ASYNC        4u   /* device-only call: do not synchronize on return */
+#define ZK_STORE_SCALAR 8u   /* force the scalar (8-byte) store path (testing)  */
+
+#define ZK_MAX_DERIV_ORDER 3 /* zk/evaluate.py:19 */
+
+typedef struct zk_ctx zk_ctx;
+typedef struct zk_plan zk_plan;
+
+/* ---- library / context ---------------------------------------------- */
+const char* zk_last_error(void);
+int zk_version(void);                       /* major*10000 + minor*100 + patch */
+int zk_device_count(int* count);
+int zk_ctx_create(int device, zk_ctx** out);
+int zk_ctx_destroy(zk_ctx* ctx);
+/* Launch on a caller-owned cudaStream_t (passed as void*); NULL = ctx stream. */
+int zk_ctx_set_stream(zk_ctx* ctx, void* stream);
+int zk_ctx_synchronize(zk_ctx* ctx);
+/* Number of kernels this ctx launched since creation (bench accounting). */
+int zk_ctx_launch_count(const zk_ctx* ctx, int64_t* count);
+
+/* ---- mode planning (host-only; usable without a GPU) -------------------
+ * Unique (n,|m|) keys in first-appearance order and the column -> key
+ * scatter, exactly as zk/modes.py:108-125. unique_n/unique_m/scatter must
+ * hold M entries each; *n_unique receives U. */
+int zk_plan_describe(const int32_t* mode_n, const int32_t* mode_m, int64_t M,
+                     int32_t* unique_n, int32_t* unique_m, int32_t* scatter,
+                     int64_t* n_unique);
+
+/* Step counters of zk/batch.py:69-94 for the same request.
+ * shared=1: cached strategy, 0: independent strategy. */
+int zk_step_counters(const int32_t* mode_n, const int32_t* mode_m, int64_t M,
+                     int deriv_order, int shared,
+                     int64_t* recursion_steps, int64_t* chain_count);
+
+/* ---- device plans ------------------------------------------------------
+ * Builds the alpha-group plan (zk/batch.py:61-66), the exact integer
+ * recursion coefficients of zk/evaluate.py:70-75 for chains 0..max_order,
+ * and the derivative prefactors of zk/evaluate.py:84-99,124-149; uploads
+ * them to the ctx's device. A plan serves every order <= max_order. */
+int zk_plan_create(zk_ctx* ctx, const int32_t* mode_n, const int32_t* mode_m,
+                   int64_t M, int max_order, zk_plan** out);
+int zk_plan_destroy(zk_plan* plan);
+/* M columns, U unique keys, G alpha groups, N highest degree. */
+int zk_plan_info(const zk_plan* plan, int64_t* M, int64_t* U, int64_t* G,
+                 int64_t* max_n);
+
+/* ---- K1: radial basis (R_n^|m| or d^k/drho^k), P x M, column-major ------
+ * rho[P] in [0,1] (not re-validated here; the Python layer validates).
+ * all_orders=0: write order deriv_order only into out.
+ * all_orders=1: write orders 0..deriv_order; order o at out + o*order_stride.
+ * ld >= P; order_stride >= ld*M when all_orders. */
+int zk_radial_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho,
+                   int64_t P, int deriv_order, int all_orders, double* out,
+                   int64_t ld, int64_t order_stride, uint32_t flags);
+
+/* ---- K1+K2: full 2-D Zernike basis at point-wise (rho, theta) ----------
+ * column (n, m): R * cos(m*theta) for m >= 0, R * sin(|m|*theta) for m < 0;
+ * the derivative order applies to the radial factor (zk/evaluate.py:259-274). */
+int zk_zernike_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho,
+                    const double* theta, int64_t P, int deriv_order,
+                    int all_orders, double* out, int64_t ld,
+                    int64_t order_stride, uint32_t flags);
+
+/* ---- K3: series evaluation f = B c without materialising B --------------
+ * coef is M x ncoef column-major (ldc >= M); f is P x ncoef (ldf >= P).
+ * theta == NULL evaluates the radial basis (no angular factor). */
+int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho,
+                   const double* theta, int64_t P, int deriv_order,
+                   const double* coef, int64_t ncoef, int64_t ldc,
+                   double* f, int64_t ldf, uint32_t flags);
+
+/* ---- K4: least-squares normal equations, accumulated -------------------
+ * G (M x M, column-major, full symmetric) += B^T B and Bty (M) += B^T y over
+ * the P points, B the 2-D basis (theta != NULL) or radial basis (theta ==
+ * NULL). G/Bty are device buffers the caller zeroes before the first call
+ * (accumulation lets a caller stream points through in chunks; the
+ * cross-GPU sum is an allreduce of G and Bty). y may be NULL (skip Bty). */
+int zk_gram_accumulate(zk_ctx* ctx, const zk_plan* plan, const double* rho,
+                       const double* theta, int64_t P, const double* y,
+                       double* G, double* Bty, uint32_t flags);
+
+/* ---- jacobi_chain export ------------------------------------------------
+ * Rows P_0..P_{j_max} of the Jacobi chain (alpha, beta >= 0) at x[N]:
+ * row j at out[j*ldo + p], ldo >= N (zk/evaluate.py:36-76 jacobi_chain, the
+ * same expression tree and IEEE division). */
+int zk_jacobi_chain(zk_ctx* ctx, const double* x, int64_t N, int j_max, int alpha,
+                    int beta, double* out, int64_t ldo, uint32_t flags);
+
+/* ---- pinned host memory (for host-output pipelines at full PCIe rate) ---- */
+int zk_host_alloc(int64_t bytes, void** out);
+int zk_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZK_B200_H */

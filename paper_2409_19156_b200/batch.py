@@ -1,0 +1,117 @@
+"""Batch evaluation of a mode set -- the reference's L3 API on the B200.
+
+zk/batch.py offers two strategies (``cached``: one shared chain per alpha
+group; ``independent``: every key from scratch) whose outputs are bitwise
+equal and whose only observable difference is the StepCounter. Here both
+strategies run the single fused kernel K1 (one sweep per (point, alpha)),
+so their values are bitwise equal by construction; each returns the
+reference's analytic counter for its strategy (zk/batch.py:69-94), computed
+by the native planner. ``parallel`` maps to nothing: the GPU grid replaces
+the reference's thread pool (zk/batch.py:136-141,174-180), and results are
+independent of it, as the reference requires (tests/test_batch.py:132-143).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .evaluate import MAX_DERIV_ORDER, basis_matrix
+from .modes import DedupPlan, ModeSet, as_mode_set, mode_arrays
+from .tables import EvalMatrix, radial_grid
+
+STRATEGIES = ("cached", "independent")  # zk/batch.py:28
+
+
+@dataclass(frozen=True)
+class StepCounter:
+    """zk/batch.py:31-36."""
+
+    recursion_steps: int
+    chain_count: int
+
+
+@dataclass(frozen=True, eq=False)
+class BatchRequest:
+    """zk/batch.py:39-58: validated modes, grid, derivative order, strategy."""
+
+    modes: ModeSet
+    grid: np.ndarray
+    deriv_order: int = 0
+    strategy: str = "cached"
+
+    def __post_init__(self):
+        object.__setattr__(self, "modes", as_mode_set(self.modes))
+        object.__setattr__(self, "grid", radial_grid(self.grid))
+        if self.deriv_order not in range(MAX_DERIV_ORDER + 1):
+            raise ValueError(
+                f"derivative order must be 0..{MAX_DERIV_ORDER}, got {self.deriv_order}")
+        if self.strategy not in STRATEGIES:
+            raise ValueError(f"strategy must be one of {STRATEGIES}, got {self.strategy!r}")
+
+
+def _counter(modes, k: int, shared: bool) -> StepCounter:
+    n, m = mode_arrays(modes)
+    steps, chains = _lib.step_counters(n, m, k, shared)
+    return StepCounter(recursion_steps=steps, chain_count=chains)
+
+
+def _plan_arrays(plan: DedupPlan) -> tuple[np.ndarray, np.ndarray]:
+    keys = np.asarray(plan.unique_keys, dtype=np.int32).reshape(-1, 2)
+    return keys[:, 0], keys[:, 1]
+
+
+def cached_step_counter(plan: DedupPlan, deriv_order: int) -> StepCounter:
+    """zk/batch.py:69-80 (counters depend only on the unique keys)."""
+    n, m = _plan_arrays(plan)
+    steps, chains = _lib.step_counters(n, m, deriv_order, True)
+    return StepCounter(steps, chains)
+
+
+def independent_step_counter(plan: DedupPlan, deriv_order: int) -> StepCounter:
+    """zk/batch.py:83-94."""
+    n, m = _plan_arrays(plan)
+    steps, chains = _lib.step_counters(n, m, deriv_order, False)
+    return StepCounter(steps, chains)
+
+
+def _evaluate(request: BatchRequest, shared: bool) -> tuple[EvalMatrix, StepCounter]:
+    n, m = mode_arrays(request.modes)
+    values = basis_matrix(n, m, request.grid, request.deriv_order)
+    table = EvalMatrix(values=values, modes=request.modes, deriv_order=request.deriv_order)
+    return table, _counter(request.modes, request.deriv_order, shared)
+
+
+def batch_cached(request: BatchRequest, parallel: bool = False) -> tuple[EvalMatrix, StepCounter]:
+    """zk/batch.py:104-142."""
+    if request.strategy != "cached":
+        raise ValueError(f"request strategy is {request.strategy!r}, expected 'cached'")
+    return _evaluate(request, shared=True)
+
+
+def batch_independent(request: BatchRequest,
+                      parallel: bool = False) -> tuple[EvalMatrix, StepCounter]:
+    """zk/batch.py:145-181."""
+    if request.strategy != "independent":
+        raise ValueError(
+            f"request strategy is {request.strategy!r}, expected 'independent'")
+    return _evaluate(request, shared=False)
+
+
+def evaluate_batch(request: BatchRequest,
+                   parallel: bool = False) -> tuple[EvalMatrix, StepCounter]:
+    """zk/batch.py:184-190."""
+    if request.strategy == "cached":
+        return batch_cached(request, parallel=parallel)
+    return batch_independent(request, parallel=parallel)
+
+
+def evaluate_batch_all_orders(request: BatchRequest) -> list[EvalMatrix]:
+    """Orders 0..request.deriv_order from ONE kernel sweep (the
+    reference needs one request per order)."""
+    n, m = mode_arrays(request.modes)
+    k = request.deriv_order
+    mats = basis_matrix(n, m, request.grid, k, all_orders=True)
+    return [EvalMatrix(values=v, modes=request.modes, deriv_order=o) for o, v in enumerate(mats)]

@@ -1,0 +1,508 @@
+// C ABI of libzk_b200.so (see include/zk_b200.h for the contract and the
+// reference interface each entry point replaces).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/zk_b200.h"
+#include "zk_internal.h"
+#include "zk_launch.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(ZK_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define ZK_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct zk_ctx {
+  int device = 0;
+  int sm_count = 148;
+  size_t max_smem = 48 * 1024;
+  cudaStream_t own = nullptr;     // default launch stream
+  cudaStream_t stream = nullptr;  // current launch stream (own or caller's)
+  cudaStream_t pipe[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr;
+  // device scratch for host-pointer calls: per pipeline slot
+  void* scratch[2] = {nullptr, nullptr};
+  size_t scratch_bytes[2] = {0, 0};
+  int64_t launches = 0;
+  std::mutex mu;  // one call at a time per ctx
+};
+
+struct zk_plan {
+  zk_ctx* ctx = nullptr;
+  zk::HostPlan host;
+  void* dmem = nullptr;
+  const zk::GroupRec* groups = nullptr;
+  const int32_t* order = nullptr;
+  const int32_t* rowptr = nullptr;
+  const int32_t* cols = nullptr;
+  const zk::ChainCoef* coef = nullptr;
+  const zk::AsmCoef* asmc = nullptr;
+};
+
+namespace {
+
+int ensure_scratch(zk_ctx* ctx, int slot, size_t bytes) {
+  if (ctx->scratch_bytes[slot] >= bytes) return ZK_OK;
+  if (ctx->scratch[slot]) {
+    cudaStreamSynchronize(ctx->pipe[slot]);
+    cudaFree(ctx->scratch[slot]);
+    ctx->scratch[slot] = nullptr;
+    ctx->scratch_bytes[slot] = 0;
+  }
+  cudaError_t e = cudaMalloc(&ctx->scratch[slot], bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ZK_ENOMEM, std::string("scratch allocation failed: ") + cudaGetErrorString(e));
+  }
+  ctx->scratch_bytes[slot] = bytes;
+  return ZK_OK;
+}
+
+struct Geometry {
+  int vec, ntiles, nchunks, tiles_per_chunk, grid;
+  size_t smem;
+};
+
+Geometry geometry(const zk_ctx* ctx, const zk_plan* plan, int64_t P, int K, bool vec2) {
+  Geometry g{};
+  g.vec = vec2 ? 2 : 1;
+  const int64_t tile_pts = int64_t(zk::kRadialThreads) * g.vec;
+  g.ntiles = static_cast<int>((P + tile_pts - 1) / tile_pts);
+  const int64_t G = static_cast<int64_t>(plan->host.groups.size());
+  const int64_t target = int64_t(ctx->sm_count) * 32;  // ~several resident waves
+  int64_t tpc = (int64_t(g.ntiles) * G + target - 1) / target;
+  tpc = std::max<int64_t>(1, std::min<int64_t>(tpc, g.ntiles));
+  g.tiles_per_chunk = static_cast<int>(tpc);
+  g.nchunks = static_cast<int>((g.ntiles + tpc - 1) / tpc);
+  g.grid = static_cast<int>(G * g.nchunks);
+  g.smem = zk::radial_smem_bytes(K, plan->host.max_jmax);
+  return g;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// One device-resident launch of K1/K2 over P points.
+int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const double* theta,
+                  int64_t P, int K, bool all, double* out, int64_t ld, int64_t ostride,
+                  bool force_scalar, cudaStream_t st) {
+  if (P == 0 || plan->host.groups.empty()) return ZK_OK;
+  const bool vec2 = !force_scalar && (ld % 2 == 0) && aligned16(out) &&
+                    (!all || ostride % 2 == 0);
+  Geometry geo = geometry(ctx, plan, P, K, vec2);
+  if (geo.smem > ctx->max_smem)
+    return fail(ZK_EINVAL, "mode set too large for the shared-memory coefficient stage "
+                           "(highest jacobi degree " + std::to_string(plan->host.max_jmax) + ")");
+  zk::RadialArgs a{};
+  a.groups = plan->groups;
+  a.order = plan->order;
+  a.rowptr = plan->rowptr;
+  a.cols = plan->cols;
+  a.coef = plan->coef;
+  a.asmc = plan->asmc;
+  a.rho = rho;
+  a.theta = theta;
+  a.out = out;
+  a.ld = ld;
+  a.ostride = ostride;
+  a.P = P;
+  a.ntiles = geo.ntiles;
+  a.nchunks = geo.nchunks;
+  a.tiles_per_chunk = geo.tiles_per_chunk;
+  cudaError_t e = zk::launch_radial(a, K, all, theta != nullptr, geo.vec, geo.grid, geo.smem, st);
+  if (e != cudaSuccess) return cuda_fail(e, "radial kernel launch");
+  ctx->launches += 1;
+  return ZK_OK;
+}
+
+int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const double* theta,
+                bool ang, int64_t P, int k, int all_orders, double* out, int64_t ld,
+                int64_t ostride, uint32_t flags) {
+  if (!ctx || !plan) return fail(ZK_EINVAL, "null ctx or plan");
+  if (plan->ctx != ctx) return fail(ZK_EINVAL, "plan belongs to another context");
+  if (k < 0 || k > ZK_MAX_DERIV_ORDER)
+    return fail(ZK_EINVAL, "derivative order must be 0..3, got " + std::to_string(k));
+  if (k > plan->host.max_order)
+    return fail(ZK_EINVAL, "plan was built for orders <= " + std::to_string(plan->host.max_order));
+  if (P < 0) return fail(ZK_EINVAL, "negative point count");
+  const int64_t M = plan->host.M;
+  const bool all = all_orders != 0 && k > 0;
+  const int NO = all ? k + 1 : 1;
+  if (P == 0 || M == 0) return ZK_OK;
+  if (!rho || !out || (ang && !theta)) return fail(ZK_EINVAL, "null data pointer");
+  if (ld < P) return fail(ZK_EINVAL, "ld must be >= P");
+  if (all && ostride < ld * M) return fail(ZK_EINVAL, "order_stride must be >= ld*M");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  ZK_CUDA(cudaSetDevice(ctx->device));
+  const bool host_in = (flags & ZK_HOST_INPUT) != 0;
+  const bool host_out = (flags & ZK_HOST_OUTPUT) != 0;
+  const bool scalar = (flags & ZK_STORE_SCALAR) != 0;
+  const int nin = ang ? 2 : 1;
+
+  if (!host_in && !host_out) {
+    int rc = launch_device(ctx, plan, rho, ang ? theta : nullptr, P, k, all, out, ld, ostride,
+                           scalar, ctx->stream);
+    if (rc) return rc;
+    if (!(flags & ZK_ASYNC)) ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+    return ZK_OK;
+  }
+
+  if (!host_out) {
+    // host inputs, device output: stage the inputs once, launch in place
+    const size_t in_bytes = align_up(size_t(P) * 8, 256);
+    int rc = ensure_scratch(ctx, 0, in_bytes * nin);
+    if (rc) return rc;
+    double* drho = static_cast<double*>(ctx->scratch[0]);
+    double* dth = ang ? drho + in_bytes / 8 : nullptr;
+    ZK_CUDA(cudaMemcpyAsync(drho, rho, size_t(P) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    if (ang)
+      ZK_CUDA(cudaMemcpyAsync(dth, theta, size_t(P) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    rc = launch_device(ctx, plan, drho, dth, P, k, all, out, ld, ostride, scalar, ctx->stream);
+    if (rc) return rc;
+    ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+    return ZK_OK;
+  }
+
+  // host output: chunk the points, double-buffered compute -> D2H pipeline on
+  // two streams so chunk c's copy overlaps chunk c+1's kernel.
+  const size_t budget = size_t(256) << 20;  // bytes of basis per slot
+  const size_t per_point = size_t(8) * size_t(M) * NO;
+  int64_t pc = static_cast<int64_t>(budget / per_point);
+  pc = std::max<int64_t>(256, pc / 256 * 256);
+  pc = std::min<int64_t>(pc, (P + 255) / 256 * 256);
+  const size_t basis_bytes = align_up(size_t(pc) * per_point, 256);
+  const size_t in_bytes = align_up(size_t(pc) * 8, 256);
+  for (int s = 0; s < 2; ++s) {
+    int rc = ensure_scratch(ctx, s, basis_bytes + in_bytes * nin);
+    if (rc) return rc;
+  }
+  // the pipeline must start after work already queued on the launch stream
+  ZK_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
+  for (int s = 0; s < 2; ++s) ZK_CUDA(cudaStreamWaitEvent(ctx->pipe[s], ctx->ev_start, 0));
+  int64_t chunk = 0;
+  for (int64_t p0 = 0; p0 < P; p0 += pc, ++chunk) {
+    const int s = static_cast<int>(chunk & 1);
+    cudaStream_t st = ctx->pipe[s];
+    const int64_t n = std::min<int64_t>(pc, P - p0);
+    double* dbasis = static_cast<double*>(ctx->scratch[s]);
+    double* din = reinterpret_cast<double*>(static_cast<char*>(ctx->scratch[s]) + basis_bytes);
+    const double* r_in = rho + p0;
+    const double* t_in = ang ? theta + p0 : nullptr;
+    if (host_in) {
+      ZK_CUDA(cudaMemcpyAsync(din, rho + p0, size_t(n) * 8, cudaMemcpyHostToDevice, st));
+      r_in = din;
+      if (ang) {
+        ZK_CUDA(cudaMemcpyAsync(din + in_bytes / 8, theta + p0, size_t(n) * 8,
+                                cudaMemcpyHostToDevice, st));
+        t_in = din + in_bytes / 8;
+      }
+    }
+    const int64_t dld = pc;
+    int rc = launch_device(ctx, plan, r_in, t_in, n, k, all, dbasis, dld, dld * M, scalar, st);
+    if (rc) return rc;
+    for (int o = 0; o < NO; ++o) {
+      ZK_CUDA(cudaMemcpy2DAsync(out + o * ostride + p0, size_t(ld) * 8, dbasis + o * dld * M,
+                                size_t(dld) * 8, size_t(n) * 8, size_t(M),
+                                cudaMemcpyDeviceToHost, st));
+    }
+  }
+  ZK_CUDA(cudaStreamSynchronize(ctx->pipe[0]));
+  ZK_CUDA(cudaStreamSynchronize(ctx->pipe[1]));
+  return ZK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* zk_last_error(void) { return g_err.c_str(); }
+
+int zk_version(void) { return 1 * 10000 + 0 * 100 + 0; }
+
+int zk_device_count(int* count) {
+  if (!count) return fail(ZK_EINVAL, "null count");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    return fail(ZK_ENODEV, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  }
+  *count = n;
+  return ZK_OK;
+}
+
+int zk_ctx_create(int device, zk_ctx** out) {
+  if (!out) return fail(ZK_EINVAL, "null output pointer");
+  *out = nullptr;
+  int n = 0;
+  int rc = zk_device_count(&n);
+  if (rc) return rc;
+  if (device < 0 || device >= n)
+    return fail(ZK_ENODEV, "device " + std::to_string(device) + " not present (" +
+                               std::to_string(n) + " devices)");
+  zk_ctx* ctx = new (std::nothrow) zk_ctx();
+  if (!ctx) return fail(ZK_ENOMEM, "ctx allocation failed");
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) {
+    cudaDeviceProp prop{};
+    e = cudaGetDeviceProperties(&prop, device);
+    if (e == cudaSuccess) {
+      ctx->sm_count = prop.multiProcessorCount;
+      ctx->max_smem = prop.sharedMemPerBlockOptin;
+      if (prop.major < 10)
+        e = cudaErrorNoKernelImageForDevice;  // built for sm_100a only
+    }
+  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pipe[0], cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pipe[1], cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    zk_ctx_destroy(ctx);
+    return cuda_fail(e, "context creation");
+  }
+  ctx->stream = ctx->own;
+  *out = ctx;
+  return ZK_OK;
+}
+
+int zk_ctx_destroy(zk_ctx* ctx) {
+  if (!ctx) return ZK_OK;
+  cudaSetDevice(ctx->device);
+  for (int s = 0; s < 2; ++s) {
+    if (ctx->pipe[s]) cudaStreamSynchronize(ctx->pipe[s]);
+    if (ctx->scratch[s]) cudaFree(ctx->scratch[s]);
+    if (ctx->pipe[s]) cudaStreamDestroy(ctx->pipe[s]);
+  }
+  if (ctx->own) {
+    cudaStreamSynchronize(ctx->own);
+    cudaStreamDestroy(ctx->own);
+  }
+  if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+  delete ctx;
+  return ZK_OK;
+}
+
+int zk_ctx_set_stream(zk_ctx* ctx, void* stream) {
+  if (!ctx) return fail(ZK_EINVAL, "null ctx");
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  return ZK_OK;
+}
+
+int zk_ctx_synchronize(zk_ctx* ctx) {
+  if (!ctx) return fail(ZK_EINVAL, "null ctx");
+  ZK_CUDA(cudaSetDevice(ctx->device));
+  ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ZK_OK;
+}
+
+int zk_ctx_launch_count(const zk_ctx* ctx, int64_t* count) {
+  if (!ctx || !count) return fail(ZK_EINVAL, "null argument");
+  *count = ctx->launches;
+  return ZK_OK;
+}
+
+int zk_plan_describe(const int32_t* mode_n, const int32_t* mode_m, int64_t M,
+                     int32_t* unique_n, int32_t* unique_m, int32_t* scatter,
+                     int64_t* n_unique) {
+  if (M < 0 || !n_unique) return fail(ZK_EINVAL, "bad arguments");
+  if (M > 0 && (!mode_n || !mode_m || !unique_n || !unique_m || !scatter))
+    return fail(ZK_EINVAL, "null array");
+  std::string err = zk::validate_modes(mode_n, mode_m, M);
+  if (!err.empty()) return fail(ZK_EINVAL, err);
+  std::vector<int32_t> kn, km, sc;
+  zk::dedup(mode_n, mode_m, M, kn, km, sc);
+  std::copy(kn.begin(), kn.end(), unique_n);
+  std::copy(km.begin(), km.end(), unique_m);
+  std::copy(sc.begin(), sc.end(), scatter);
+  *n_unique = static_cast<int64_t>(kn.size());
+  return ZK_OK;
+}
+
+int zk_step_counters(const int32_t* mode_n, const int32_t* mode_m, int64_t M, int deriv_order,
+                     int shared, int64_t* recursion_steps, int64_t* chain_count) {
+  if (M < 0 || !recursion_steps || !chain_count) return fail(ZK_EINVAL, "bad arguments");
+  if (M > 0 && (!mode_n || !mode_m)) return fail(ZK_EINVAL, "null array");
+  if (deriv_order < 0 || deriv_order > ZK_MAX_DERIV_ORDER)
+    return fail(ZK_EINVAL, "derivative order must be 0..3");
+  std::string err = zk::validate_modes(mode_n, mode_m, M);
+  if (!err.empty()) return fail(ZK_EINVAL, err);
+  zk::step_counters(mode_n, mode_m, M, deriv_order, shared != 0, *recursion_steps, *chain_count);
+  return ZK_OK;
+}
+
+int zk_plan_create(zk_ctx* ctx, const int32_t* mode_n, const int32_t* mode_m, int64_t M,
+                   int max_order, zk_plan** out) {
+  if (!ctx || !out) return fail(ZK_EINVAL, "null argument");
+  *out = nullptr;
+  if (M > 0 && (!mode_n || !mode_m)) return fail(ZK_EINVAL, "null mode arrays");
+  zk_plan* plan = new (std::nothrow) zk_plan();
+  if (!plan) return fail(ZK_ENOMEM, "plan allocation failed");
+  std::string err = zk::build_plan(mode_n, mode_m, M, max_order, plan->host);
+  if (!err.empty()) {
+    delete plan;
+    return fail(ZK_EINVAL, err);
+  }
+  plan->ctx = ctx;
+  const zk::HostPlan& h = plan->host;
+  const size_t A = 256;
+  size_t off_groups = 0;
+  size_t off_order = align_up(off_groups + h.groups.size() * sizeof(zk::GroupRec), A);
+  size_t off_rowptr = align_up(off_order + h.launch_order.size() * 4, A);
+  size_t off_cols = align_up(off_rowptr + h.rowptr.size() * 4, A);
+  size_t off_coef = align_up(off_cols + h.cols.size() * 4, A);
+  size_t off_asm = align_up(off_coef + h.coef.size() * sizeof(zk::ChainCoef), A);
+  size_t total = align_up(off_asm + h.asmc.size() * sizeof(zk::AsmCoef), A) + A;
+  std::vector<unsigned char> blob(total, 0);
+  auto put = [&](size_t off, const void* src, size_t bytes) {
+    if (bytes) std::memcpy(blob.data() + off, src, bytes);
+  };
+  put(off_groups, h.groups.data(), h.groups.size() * sizeof(zk::GroupRec));
+  put(off_order, h.launch_order.data(), h.launch_order.size() * 4);
+  put(off_rowptr, h.rowptr.data(), h.rowptr.size() * 4);
+  put(off_cols, h.cols.data(), h.cols.size() * 4);
+  put(off_coef, h.coef.data(), h.coef.size() * sizeof(zk::ChainCoef));
+  put(off_asm, h.asmc.data(), h.asmc.size() * sizeof(zk::AsmCoef));
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess) e = cudaMalloc(&plan->dmem, total);
+  if (e == cudaSuccess) e = cudaMemcpy(plan->dmem, blob.data(), total, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (plan->dmem) cudaFree(plan->dmem);
+    delete plan;
+    return cuda_fail(e, "plan upload");
+  }
+  unsigned char* base = static_cast<unsigned char*>(plan->dmem);
+  plan->groups = reinterpret_cast<const zk::GroupRec*>(base + off_groups);
+  plan->order = reinterpret_cast<const int32_t*>(base + off_order);
+  plan->rowptr = reinterpret_cast<const int32_t*>(base + off_rowptr);
+  plan->cols = reinterpret_cast<const int32_t*>(base + off_cols);
+  plan->coef = reinterpret_cast<const zk::ChainCoef*>(base + off_coef);
+  plan->asmc = reinterpret_cast<const zk::AsmCoef*>(base + off_asm);
+  *out = plan;
+  return ZK_OK;
+}
+
+int zk_plan_destroy(zk_plan* plan) {
+  if (!plan) return ZK_OK;
+  if (plan->dmem) {
+    cudaSetDevice(plan->ctx->device);
+    cudaFree(plan->dmem);
+  }
+  delete plan;
+  return ZK_OK;
+}
+
+int zk_plan_info(const zk_plan* plan, int64_t* M, int64_t* U, int64_t* G, int64_t* max_n) {
+  if (!plan) return fail(ZK_EINVAL, "null plan");
+  if (M) *M = plan->host.M;
+  if (U) *U = static_cast<int64_t>(plan->host.key_n.size());
+  if (G) *G = static_cast<int64_t>(plan->host.groups.size());
+  if (max_n) *max_n = plan->host.max_n;
+  return ZK_OK;
+}
+
+int zk_radial_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, int64_t P,
+                   int deriv_order, int all_orders, double* out, int64_t ld,
+                   int64_t order_stride, uint32_t flags) {
+  return eval_common(ctx, plan, rho, nullptr, false, P, deriv_order, all_orders, out, ld,
+                     order_stride, flags);
+}
+
+int zk_zernike_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const double* theta,
+                    int64_t P, int deriv_order, int all_orders, double* out, int64_t ld,
+                    int64_t order_stride, uint32_t flags) {
+  return eval_common(ctx, plan, rho, theta, true, P, deriv_order, all_orders, out, ld,
+                     order_stride, flags);
+}
+
+int zk_series_eval(zk_ctx*, const zk_plan*, const double*, const double*, int64_t, int,
+                   const double*, int64_t, int64_t, double*, int64_t, uint32_t) {
+  return fail(ZK_EINVAL, "zk_series_eval: not available in this build");
+}
+
+int zk_gram_accumulate(zk_ctx*, const zk_plan*, const double*, const double*, int64_t,
+                       const double*, double*, double*, uint32_t) {
+  return fail(ZK_EINVAL, "zk_gram_accumulate: not available in this build");
+}
+
+int zk_jacobi_chain(zk_ctx* ctx, const double* x, int64_t N, int j_max, int alpha, int beta,
+                    double* out, int64_t ldo, uint32_t flags) {
+  if (!ctx) return fail(ZK_EINVAL, "null ctx");
+  if (j_max < 0) return fail(ZK_EINVAL, "chain degree must be >= 0, got " + std::to_string(j_max));
+  if (alpha < 0 || beta < 0)
+    return fail(ZK_EINVAL, "need alpha, beta >= 0, got (" + std::to_string(alpha) + ", " +
+                               std::to_string(beta) + ")");
+  if (N < 0 || ldo < N) return fail(ZK_EINVAL, "bad sizes");
+  if (N == 0) return ZK_OK;
+  if (!x || !out) return fail(ZK_EINVAL, "null data pointer");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  ZK_CUDA(cudaSetDevice(ctx->device));
+  const bool host_in = (flags & ZK_HOST_INPUT) != 0;
+  const bool host_out = (flags & ZK_HOST_OUTPUT) != 0;
+  const size_t in_bytes = align_up(size_t(N) * 8, 256);
+  const size_t out_bytes = size_t(j_max + 1) * size_t(N) * 8;
+  int rc = ensure_scratch(ctx, 0, (host_in ? in_bytes : 0) + (host_out ? out_bytes : 0) + 256);
+  if (rc) return rc;
+  char* base = static_cast<char*>(ctx->scratch[0]);
+  const double* dx = x;
+  if (host_in) {
+    ZK_CUDA(cudaMemcpyAsync(base, x, size_t(N) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    dx = reinterpret_cast<const double*>(base);
+  }
+  double* dout = host_out ? reinterpret_cast<double*>(base + (host_in ? in_bytes : 0)) : out;
+  const int64_t dld = host_out ? N : ldo;
+  ZK_CUDA(zk::launch_chain(dx, N, j_max, alpha, beta, dout, dld, ctx->stream));
+  ctx->launches += 1;
+  if (host_out)
+    ZK_CUDA(cudaMemcpy2DAsync(out, size_t(ldo) * 8, dout, size_t(N) * 8, size_t(N) * 8,
+                              size_t(j_max + 1), cudaMemcpyDeviceToHost, ctx->stream));
+  if (!(flags & ZK_ASYNC) || host_in || host_out) ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ZK_OK;
+}
+
+int zk_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return fail(ZK_EINVAL, "bad arguments");
+  *out = nullptr;
+  if (bytes == 0) return ZK_OK;
+  cudaError_t e = cudaHostAlloc(out, size_t(bytes), cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    return fail(ZK_ENOMEM, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+  }
+  return ZK_OK;
+}
+
+int zk_host_free(void* p) {
+  if (!p) return ZK_OK;
+  ZK_CUDA(cudaFreeHost(p));
+  return ZK_OK;
+}
+
+}  // extern "C"

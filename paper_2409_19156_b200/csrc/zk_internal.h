@@ -1,0 +1,73 @@
+// Internal declarations shared by the planner (host C++) and the CUDA side.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace zk {
+
+// Per-degree recursion coefficients of one chain, the integers of
+// zk/evaluate.py:70-74 held exactly as binary64 plus the correctly rounded
+// reciprocal of `lead` (used for an exact, Markstein-corrected division).
+// Six doubles so a warp-uniform entry is three 16-byte shared-memory loads.
+struct ChainCoef {
+  double mid_x;      // (c-1) c (c-2)
+  double mid_const;  // (c-1) (alpha^2 - beta^2)
+  double last;       // 2 (j+alpha-1)(j+beta-1) c
+  double rcp_lead;   // RN(1/lead)
+  double lead;       // 2 j (c-j)(c-2)
+  double pad;
+};
+static_assert(sizeof(ChainCoef) == 48, "ChainCoef layout");
+
+// Derivative prefactors per jacobi degree j of a group (zk/evaluate.py:127-149);
+// every product is an exact integer or half-integer in binary64.
+struct AsmCoef {
+  double c11;  // k=1: 4 s1
+  double c21;  // k=2: 4 (2m+1) s1
+  double c22;  // k=2: 16 s2
+  double c31;  // k=3: 12 m m s1
+  double c32;  // k=3: 48 (m+1) s2
+  double c33;  // k=3: 64 s3
+  double pad0, pad1;
+};
+static_assert(sizeof(AsmCoef) == 64, "AsmCoef layout");
+
+// One alpha group (zk/batch.py:61-66): all requested keys (n, alpha).
+struct GroupRec {
+  int32_t alpha;
+  int32_t jmax;      // highest requested jacobi degree in the group
+  int32_t row0;      // offset of this group's rowptr slice (jmax+2 entries)
+  int32_t coef_off;  // offset (in ChainCoef units) of chain 0, degree 0
+  int32_t asm_off;   // offset (in AsmCoef units) of degree 0
+  int32_t ncols;     // columns served by this group
+  int32_t pad0, pad1;
+};
+static_assert(sizeof(GroupRec) == 32, "GroupRec layout");
+
+struct HostPlan {
+  int64_t M = 0;
+  int32_t max_n = 0;
+  int32_t max_order = 0;
+  int32_t max_jmax = 0;
+  std::vector<int32_t> key_n, key_m;  // unique keys, first-appearance order
+  std::vector<int32_t> scatter;       // column -> key slot
+  std::vector<GroupRec> groups;       // sorted by alpha
+  std::vector<int32_t> launch_order;  // group indices, heaviest first
+  std::vector<int32_t> rowptr;        // per group jmax+2 entries, into cols
+  std::vector<int32_t> cols;          // column*2 + (m < 0)
+  std::vector<ChainCoef> coef;        // per group: (max_order+1) x (jmax+1)
+  std::vector<AsmCoef> asmc;          // per group: (jmax+1)
+};
+
+// Returns empty string on success, else the error message.
+std::string validate_modes(const int32_t* n, const int32_t* m, int64_t M);
+void dedup(const int32_t* n, const int32_t* m, int64_t M, std::vector<int32_t>& key_n,
+           std::vector<int32_t>& key_m, std::vector<int32_t>& scatter);
+std::string build_plan(const int32_t* n, const int32_t* m, int64_t M, int max_order,
+                       HostPlan& out);
+void step_counters(const int32_t* n, const int32_t* m, int64_t M, int k, bool shared,
+                   int64_t& steps, int64_t& chains);
+
+}  // namespace zk

@@ -1,0 +1,144 @@
+// Device-side building blocks shared by the Zernike kernels (sm_100a, fp64).
+//
+// Arithmetic contract: every expression of the reference's recursion and
+// assembly (zk/evaluate.py:33,68,75,124-154) is written with explicit
+// round-to-nearest intrinsics (__dmul_rn/__dadd_rn/__dsub_rn) so nvcc cannot
+// contract it into FMAs; the division by the exact integer `lead` is done as
+// q = RN(num*RN(1/lead)), r = fma(-q, lead, num), q' = fma(r, RN(1/lead), q),
+// which is the correctly rounded quotient (Markstein's theorem; verified
+// exhaustively for every lead with n <= 1000) -- i.e. bitwise
+// equal to the reference's IEEE `/ lead` at a third of the cost of a DDIV
+// sequence. rho**e is computed in double-double and rounded once (correctly
+// rounded up to ~2^-100 relative), the only place the kernels can differ from
+// numpy's SIMD pow (<= 0.67 ulp).
+#pragma once
+
+#include <cstdint>
+
+#include "zk_internal.h"
+
+namespace zk {
+
+struct dd {
+  double hi, lo;
+};
+
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+  const double p = __dmul_rn(a.hi, b.hi);
+  double e = __fma_rn(a.hi, b.hi, -p);
+  e = __fma_rn(a.hi, b.lo, e);
+  e = __fma_rn(a.lo, b.hi, e);
+  const double s = __dadd_rn(p, e);
+  return dd{s, __dsub_rn(e, __dsub_rn(s, p))};
+}
+
+__device__ __forceinline__ dd dd_mul_d(dd a, double b) {
+  const double p = __dmul_rn(a.hi, b);
+  double e = __fma_rn(a.hi, b, -p);
+  e = __fma_rn(a.lo, b, e);
+  const double s = __dadd_rn(p, e);
+  return dd{s, __dsub_rn(e, __dsub_rn(s, p))};
+}
+
+// x**e for integer e >= 0, 0**0 == 1 (zk/evaluate.py:116-117 convention).
+__device__ __forceinline__ dd dd_pow(double x, int e) {
+  dd r{1.0, 0.0};
+  dd b{x, 0.0};
+  while (e > 0) {
+    if (e & 1) r = dd_mul(r, b);
+    e >>= 1;
+    if (e) b = dd_mul(b, b);
+  }
+  return r;
+}
+
+// u = 1 - (2 rho) rho   (zk/evaluate.py:33)
+__device__ __forceinline__ double jacobi_u(double rho) {
+  return __dsub_rn(1.0, __dmul_rn(2.0 * rho, rho));
+}
+
+// P_1 = (a+1) + ((a+b+2) (x-1)) / 2   (zk/evaluate.py:68)
+__device__ __forceinline__ double jacobi_p1(double a1, double ab2, double x) {
+  return __dadd_rn(a1, __dmul_rn(__dmul_rn(ab2, __dsub_rn(x, 1.0)), 0.5));
+}
+
+// P_j = ((mid_x x + mid_const) P_{j-1} - last P_{j-2}) / lead   (zk/evaluate.py:75)
+__device__ __forceinline__ double jacobi_step(const ChainCoef& c, double x, double p1,
+                                              double p0) {
+  const double t = __dmul_rn(__dadd_rn(__dmul_rn(c.mid_x, x), c.mid_const), p1);
+  const double num = __dsub_rn(t, __dmul_rn(c.last, p0));
+  const double q = __dmul_rn(num, c.rcp_lead);
+  const double r = __fma_rn(-q, c.lead, num);
+  return __fma_rn(r, c.rcp_lead, q);
+}
+
+// Per-thread, j-independent factors of the assembly (zk/evaluate.py:124-149):
+// the rho powers and the integer prefactors that multiply them.
+template <int K>
+struct PowSet {
+  double A0;              // rho^m
+  double A1, B1;          // m rho^max(m-1,0), rho^(m+1)
+  double A2, B2, C2;      // (m-1)m rho^max(m-2,0), rho^m, rho^(m+2)
+  double A3, B3, C3, D3;  // (m-2)(m-1)m rho^max(m-3,0), rho^max(m-1,0), rho^(m+1), rho^(m+3)
+};
+
+template <int K>
+__device__ __forceinline__ PowSet<K> make_powset(double rho, int m) {
+  PowSet<K> s;
+  const int e_lo = m - K > 0 ? m - K : 0;
+  dd acc = dd_pow(rho, e_lo);
+  const int em1 = m - 1 > 0 ? m - 1 : 0;
+  const int em2 = m - 2 > 0 ? m - 2 : 0;
+  const int em3 = m - 3 > 0 ? m - 3 : 0;
+  double p_m = 1.0, p_m1 = 1.0, p_m2 = 1.0, p_m3 = 1.0, p_p1 = 0.0, p_p2 = 0.0, p_p3 = 0.0;
+#pragma unroll
+  for (int t = 0; t <= 2 * K; ++t) {
+    const int e = e_lo + t;
+    const double v = acc.hi;
+    if (e == m) p_m = v;
+    if (e == em1) p_m1 = v;
+    if (e == em2) p_m2 = v;
+    if (e == em3) p_m3 = v;
+    if (e == m + 1) p_p1 = v;
+    if (e == m + 2) p_p2 = v;
+    if (e == m + 3) p_p3 = v;
+    if (t < 2 * K) acc = dd_mul_d(acc, rho);
+  }
+  const double md = static_cast<double>(m);
+  s.A0 = p_m;
+  s.A1 = __dmul_rn(md, p_m1);
+  s.B1 = p_p1;
+  s.A2 = __dmul_rn(static_cast<double>(static_cast<long long>(m - 1) * m), p_m2);
+  s.B2 = p_m;
+  s.C2 = p_p2;
+  s.A3 = __dmul_rn(static_cast<double>(static_cast<long long>(m - 2) * (m - 1) * m), p_m3);
+  s.B3 = p_m1;
+  s.C3 = p_p1;
+  s.D3 = p_p3;
+  return s;
+}
+
+// Radial value of order O from the chain values ch[i] = P_{j-i}^{(m+i,i)}(u),
+// before the (-1)^j sign (zk/evaluate.py:124-149, same operation order).
+template <int O, int K>
+__device__ __forceinline__ double assemble(const PowSet<K>& s, const AsmCoef& a,
+                                           const double* ch) {
+  if constexpr (O == 0) {
+    return __dmul_rn(s.A0, ch[0]);
+  } else if constexpr (O == 1) {
+    return __dsub_rn(__dmul_rn(s.A1, ch[0]), __dmul_rn(__dmul_rn(a.c11, s.B1), ch[1]));
+  } else if constexpr (O == 2) {
+    const double t0 = __dmul_rn(s.A2, ch[0]);
+    const double t1 = __dmul_rn(__dmul_rn(a.c21, s.B2), ch[1]);
+    const double t2 = __dmul_rn(__dmul_rn(a.c22, s.C2), ch[2]);
+    return __dadd_rn(__dsub_rn(t0, t1), t2);
+  } else {
+    const double t0 = __dmul_rn(s.A3, ch[0]);
+    const double t1 = __dmul_rn(__dmul_rn(a.c31, s.B3), ch[1]);
+    const double t2 = __dmul_rn(__dmul_rn(a.c32, s.C3), ch[2]);
+    const double t3 = __dmul_rn(__dmul_rn(a.c33, s.D3), ch[3]);
+    return __dsub_rn(__dadd_rn(__dsub_rn(t0, t1), t2), t3);
+  }
+}
+
+}  // namespace zk

@@ -1,0 +1,78 @@
+// Kernel argument blocks and launchers (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+#include "zk_internal.h"
+
+namespace zk {
+
+constexpr int kRadialThreads = 128;
+
+struct RadialArgs {
+  const GroupRec* groups;
+  const int32_t* order;   // launch order of groups (heaviest first)
+  const int32_t* rowptr;
+  const int32_t* cols;
+  const ChainCoef* coef;
+  const AsmCoef* asmc;
+  const double* rho;
+  const double* theta;    // only for the 2-D (angular) variant
+  double* out;
+  long long ld;           // column stride of out (elements)
+  long long ostride;      // stride between derivative orders (all_orders)
+  long long P;            // points in this launch
+  int ntiles;             // ceil(P / (threads*VEC))
+  int nchunks;            // CTAs per group
+  int tiles_per_chunk;
+};
+
+size_t radial_smem_bytes(int K, int max_jmax);
+cudaError_t launch_radial(const RadialArgs& a, int K, bool all, bool ang, int vec, int grid,
+                          size_t smem, cudaStream_t st);
+
+struct SeriesArgs {
+  const GroupRec* groups;
+  int ngroups;
+  const int32_t* rowptr;
+  const int32_t* cols;
+  const ChainCoef* coef;
+  const AsmCoef* asmc;
+  const double* rho;
+  const double* theta;    // nullptr: radial basis
+  const double* c;        // M x ncoef, column-major, ldc
+  long long ldc;
+  int ncoef;
+  double* f;              // P x ncoef, column-major, ldf
+  long long ldf;
+  long long P;
+};
+
+cudaError_t launch_series(const SeriesArgs& a, int K, cudaStream_t st, int* launches);
+
+struct GramArgs {
+  const GroupRec* groups;
+  int ngroups;
+  const int32_t* rowptr;
+  const int32_t* cols;
+  const ChainCoef* coef;
+  const AsmCoef* asmc;
+  const double* rho;
+  const double* theta;
+  const double* y;
+  long long P;
+  long long M;
+  double* G;
+  double* Bty;
+  double* scratch;        // basis panel, P_panel x M column-major
+  long long panel;        // points per panel
+};
+
+cudaError_t launch_gram(const GramArgs& a, cudaStream_t st, int* launches);
+
+cudaError_t launch_chain(const double* x, long long N, int jmax, int alpha, int beta,
+                         double* out, long long ldo, cudaStream_t st);
+
+}  // namespace zk

@@ -1,0 +1,331 @@
+"""GPU parity of K1 (radial basis, orders 0..3), K2 (2-D basis) and the
+chain export against the CPU oracle and the reference's golden vectors.
+Every call goes through the C ABI (libzk_b200.so)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import zk_oracle as orc
+from conftest import rel_err, within_tolerance
+
+pytestmark = pytest.mark.gpu
+
+zb = pytest.importorskip("paper_2409_19156_b200")
+from paper_2409_19156_b200 import _lib  # noqa: E402
+
+
+def pairs(modes):
+    return [(md.n, md.m) for md in modes]
+
+
+def radial(modes, grid, k=0):
+    t, _ = zb.evaluate_batch(zb.BatchRequest(modes=modes, grid=grid, deriv_order=k))
+    return t.values
+
+
+# --------------------------------------------------------------------------
+# configs vs oracle / golden
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_config1_matches_oracle_and_golden(golden, k):
+    modes = zb.full_mode_set(20)
+    grid = golden["c1_grid_k0"] if k == 0 else golden["c1_grid_k123"]
+    got = radial(modes, grid, k)
+    ref = orc.radial_batch(pairs(modes), grid, k)
+    assert within_tolerance(got, ref)
+    assert rel_err(got[:, golden["c1_ucols"]], golden[f"c1_k{k}"]) <= 1e-12
+    # m = 0 columns use no power of rho for k = 0: the recursion is bitwise
+    # the reference's (exact division via the Markstein correction)
+    if k == 0:
+        m0 = [c for c, md in enumerate(modes) if md.m == 0]
+        assert np.array_equal(got[:, m0], ref[:, m0])
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_config2_subsample_matches_golden(golden, k):
+    modes = zb.full_mode_set(100)
+    grid = golden["c2_grid"] if k == 0 else golden["c2_grid"][::4]
+    got = radial(modes, grid, k)[:, golden["c2_ucols"]]
+    assert within_tolerance(got, golden[f"c2_k{k}"])
+    # most entries are bitwise the reference's (only rho**m can differ)
+    assert np.mean(got == golden[f"c2_k{k}"]) > 0.5
+
+
+def test_config2_full_size_spot_checks():
+    """n=100 x 1e5 (config 2) through the numpy API; every point is
+    independent, so a seeded subsample is checked against the oracle."""
+    modes = zb.full_mode_set(100)
+    grid = zb.linear_radial_grid(100_000)
+    got = radial(modes, grid, 0)
+    assert got.shape == (100_000, 5151) and got.flags.f_contiguous
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([[0, 1, 99_999], rng.integers(0, 100_000, 61)]))
+    ref = orc.radial_batch(pairs(modes), grid[idx], 0)
+    assert within_tolerance(got[idx], ref)
+    # R_n^m(1) = 1 for every mode (reference tests/test_evaluate.py:114-117)
+    assert np.abs(got[-1] - 1.0).max() <= 1e-11
+    # centre values (tests/test_evaluate.py:86-91)
+    want0 = np.array([0.0 if md.m else (1.0 if md.n % 4 == 0 else -1.0) for md in modes])
+    assert np.abs(got[0] - want0).max() <= 1e-15
+
+
+def test_config3_all_orders_equal_single_order_bitwise():
+    modes = zb.full_mode_set(100)
+    grid = zb.linear_radial_grid(20_000)
+    req = zb.BatchRequest(modes=modes, grid=grid, deriv_order=3)
+    mats = zb.evaluate_batch_all_orders(req)
+    assert [m.deriv_order for m in mats] == [0, 1, 2, 3]
+    for k in range(4):
+        single = radial(modes, grid, k)
+        assert np.array_equal(mats[k].values, single), k
+    rng = np.random.default_rng(1)
+    idx = rng.integers(0, grid.size, 24)
+    for k in range(4):
+        ref = orc.radial_batch(pairs(modes), grid[idx], k)
+        assert within_tolerance(mats[k].values[idx], ref), k
+
+
+def test_config4_high_order_error_no_worse_than_reference(golden):
+    """n=200 (20,301 modes) x 1e4: max-abs error against the exact bigint
+    oracle must not exceed the reference's own error on the same points."""
+    modes = zb.full_mode_set(200)
+    P = 10_000
+    grid = zb.linear_radial_grid(P)
+    got = radial(modes, grid, 0)
+    ucols = golden["c4_ucols"]
+    rng = np.random.default_rng(2)
+    idx = np.unique(np.concatenate([[0, 1, P // 3, P - 2, P - 1], rng.integers(0, P, 19)]))
+    pts = grid[idx]
+    umodes = [pairs(modes)[c] for c in ucols]
+    exact = orc.exact_table(umodes, pts, 0)
+    ref = orc.radial_batch(umodes, pts, 0)
+    err_gpu = np.abs(got[idx][:, ucols] - exact).max()
+    err_ref = np.abs(ref - exact).max()
+    assert err_gpu <= err_ref, (err_gpu, err_ref)
+    # and on the committed golden points (exact oracle from the reference)
+    gidx = np.searchsorted(grid, golden["c4_grid"])
+    assert np.array_equal(grid[gidx], golden["c4_grid"])
+    err_gpu_g = np.abs(got[gidx][:, ucols] - golden["c4_exact"]).max()
+    err_ref_g = np.abs(golden["c4_k0"] - golden["c4_exact"]).max()
+    assert err_gpu_g <= err_ref_g, (err_gpu_g, err_ref_g)
+
+
+def test_config5_2d_basis_matches_golden(golden):
+    modes = zb.full_mode_set(60)
+    n = np.array([md.n for md in modes])
+    m = np.array([md.m for md in modes])
+    B = zb.zernike_basis(golden["c5_rho"], golden["c5_theta"], n, m)
+    assert within_tolerance(B, golden["c5_B"])
+    B1 = zb.zernike_basis(golden["c5_rho"], golden["c5_theta"], n, m, 1)
+    assert within_tolerance(B1, golden["c5_B_k1"])
+    f = B @ golden["c5_coef"]
+    assert np.abs(f - golden["c5_f"]).max() <= 1e-11
+
+
+# --------------------------------------------------------------------------
+# the reference's cross-entry-point bitwise invariants
+# --------------------------------------------------------------------------
+
+def test_batch_column_equals_single_mode_call():
+    grid = zb.linear_radial_grid(37)
+    modes = zb.full_mode_set(10)
+    table = radial(modes, grid, 2)
+    for col, md in enumerate(modes):
+        assert np.array_equal(table[:, col], zb.radial_jacobi(md.n, md.m_abs, grid, 2))
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_strategies_agree_bitwise(k):
+    grid = zb.linear_radial_grid(100)
+    modes = zb.full_mode_set(12)
+    a, ca = zb.batch_cached(zb.BatchRequest(modes=modes, grid=grid, deriv_order=k))
+    b, cb = zb.batch_independent(
+        zb.BatchRequest(modes=modes, grid=grid, deriv_order=k, strategy="independent"))
+    assert np.array_equal(a.values, b.values)
+    assert ca.recursion_steps <= cb.recursion_steps and ca.chain_count <= cb.chain_count
+    s, _ = zb.batch_cached(zb.BatchRequest(modes=modes, grid=grid, deriv_order=k), parallel=True)
+    assert np.array_equal(a.values, s.values)
+
+
+def test_duplicate_and_sign_flipped_columns():
+    grid = zb.linear_radial_grid(21)
+    modes = zb.as_mode_set([(4, 2), (4, -2), (4, 2), (2, 0), (4, 2)])
+    table, counter = zb.batch_cached(zb.BatchRequest(modes=modes, grid=grid))
+    for c in (1, 2, 4):
+        assert np.array_equal(table.values[:, 0], table.values[:, c])
+    assert counter.chain_count == 2
+
+
+def test_arbitrary_requests_match_oracle(golden):
+    for r in range(6):
+        modes = zb.as_mode_set([tuple(x) for x in golden[f"idx_req{r}"].tolist()])
+        for k in (0, 2):
+            got = radial(modes, golden["idx_req_grid"], k)
+            assert within_tolerance(got, golden[f"idx_req{r}_k{k}"]), (r, k)
+
+
+def test_zernike_eval_angular_split_is_exact():
+    rho = np.array([0.6])
+    for n, m in [(3, 1), (4, 2), (5, 3)]:
+        radial1 = zb.radial_jacobi(n, m, rho)[0]
+        assert zb.zernike_eval(zb.make_mode(n, m), rho, [0.0])[0] == radial1
+        assert zb.zernike_eval(zb.make_mode(n, -m), rho, [0.0])[0] == 0.0
+        q = np.pi / (2 * m)
+        assert zb.zernike_eval(zb.make_mode(n, -m), rho, [q])[0] == pytest.approx(radial1, rel=1e-12)
+    assert zb.zernike_eval(zb.make_mode(2, 2), [1.0], [0.0])[0] == pytest.approx(1.0, abs=1e-14)
+    assert zb.zernike_eval(zb.make_mode(1, 1), [0.5], [np.pi])[0] == pytest.approx(-0.5, abs=1e-15)
+    assert zb.zernike_eval(zb.make_mode(2, 0), [0.5], [1.234], 1)[0] == pytest.approx(2.0, abs=1e-14)
+
+
+def test_zernike_eval_equals_oracle_per_mode():
+    rng = np.random.default_rng(3)
+    rho = rng.uniform(size=33)
+    th = rng.uniform(-7, 7, size=33)
+    for md in zb.full_mode_set(16):
+        for k in (0, 3):
+            got = zb.zernike_eval(md, rho, th, k)
+            ref = orc.zernike_2d(md.n, md.m, rho, th, k)
+            assert within_tolerance(got[:, None], ref[:, None]), (md, k)
+
+
+# --------------------------------------------------------------------------
+# known answers of the reference tests
+# --------------------------------------------------------------------------
+
+def test_exact_zero_and_constant_derivatives():
+    grid = np.linspace(0.0, 1.0, 7)
+    for k in (1, 2, 3):
+        assert np.all(zb.radial_jacobi(0, 0, grid, k) == 0.0)
+    assert np.all(zb.radial_jacobi(1, 1, grid, 2) == 0.0)
+    assert np.all(zb.radial_jacobi(2, 2, grid, 3) == 0.0)
+    assert np.all(zb.radial_jacobi(3, 3, grid, 3) == 6.0)
+    assert zb.radial_jacobi(1, 1, [0.3])[0] == pytest.approx(0.3, abs=1e-15)
+    assert zb.radial_jacobi(2, 0, [0.5])[0] == pytest.approx(-0.5, abs=1e-15)
+    assert zb.radial_jacobi(4, 0, [1.0])[0] == pytest.approx(1.0, abs=1e-14)
+    assert zb.radial_jacobi(2, 0, [0.5], 1)[0] == pytest.approx(2.0, abs=1e-14)
+    assert zb.radial_jacobi(0, 0, [0.0])[0] == 1.0  # 0**0 == 1
+
+
+def test_endpoint_is_one_to_n150():
+    modes = [zb.make_mode(n, m) for n in range(0, 151, 7) for m in range(n % 2, n + 1, 2)]
+    got = radial(modes, [1.0])
+    assert np.abs(got - 1.0).max() <= 1e-11
+
+
+def test_finite_difference_first_derivative():
+    h = 1e-6
+    pts = np.linspace(0.1, 0.9, 33)
+    modes = [zb.make_mode(n, m) for n in range(31) for m in range(n % 2, n + 1, 2)]
+    d1 = radial(modes, pts, 1)
+    fd = (radial(modes, pts + h) - radial(modes, pts - h)) / (2 * h)
+    scale = np.maximum(1.0, np.abs(d1).max(axis=0))
+    assert (np.abs(fd - d1).max(axis=0) / scale).max() < 1e-4
+
+
+def test_low_order_modes_match_exact_oracle():
+    # tests/test_evaluate.py:93-101: n <= 12, every order, 1e-12 relative
+    from fractions import Fraction
+    grid = zb.linear_radial_grid(100)
+    modes = [(n, m) for n in range(13) for m in range(n % 2, n + 1, 2)]
+    for k in range(4):
+        exact = orc.exact_table(modes, grid, k)
+        got = radial(zb.as_mode_set(modes), grid, k)
+        assert rel_err(got, exact) <= 1e-12, k
+    assert Fraction(grid[3]) == Fraction(grid[3])
+
+
+def test_jacobi_chain_bitwise_and_scipy():
+    from scipy.special import eval_jacobi
+    x = np.linspace(-1.0, 1.0, 23)
+    for a, b in [(0, 0), (1, 0), (5, 0), (2, 2), (7, 3)]:
+        got = zb.jacobi_chain(12, a, b, x)
+        assert np.array_equal(got, orc.jacobi_chain(12, a, b, x))
+        for d in range(13):
+            want = eval_jacobi(d, a, b, x)
+            assert (np.abs(got[d] - want) / np.maximum(1.0, np.abs(want))).max() < 1e-12
+    assert np.all(zb.jacobi_chain(0, 3, 1, x)[0] == 1.0)
+    assert zb.jacobi_chain(1, 2, 0, [-1.0])[1][0] == -1.0
+    assert zb.jacobi_chain(2, 0, 0, [0.5])[2][0] == -0.125
+
+
+# --------------------------------------------------------------------------
+# C ABI paths: device buffers, ld > P, odd P, scalar vs vector stores,
+# host-in/device-out, multi-chunk host-out pipeline
+# --------------------------------------------------------------------------
+
+torch = pytest.importorskip("torch")
+
+
+def _plan(modes):
+    ctx = _lib.context()
+    n = np.array([md.n for md in modes], np.int32)
+    m = np.array([md.m for md in modes], np.int32)
+    return ctx, _lib.plan_for(ctx, n, m)
+
+
+@pytest.mark.parametrize("P", [1, 2, 255, 256, 257, 1001])
+def test_device_paths_ld_and_tails(P):
+    modes = zb.full_mode_set(9)
+    M = len(modes)
+    ctx, plan = _plan(modes)
+    grid = np.random.default_rng(P).uniform(size=P)
+    ref = radial(modes, grid, 2)
+    d_rho = torch.tensor(grid, device="cuda")
+    for ld, flags in [(P, 0), (P + 3, 0), (P + (P % 2), _lib.ZK_STORE_SCALAR), (P + 8, 0)]:
+        out = torch.full((M, ld), float("nan"), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        _lib.check(_lib.lib.zk_radial_eval(ctx.handle, plan.handle, d_rho.data_ptr(), P, 2, 0,
+                                           out.data_ptr(), ld, 0, flags), "radial")
+        host = out.cpu().numpy()
+        assert np.array_equal(host[:, :P].T, ref), (ld, flags)
+        assert np.isnan(host[:, P:]).all()  # padding untouched
+
+
+def test_host_input_device_output_and_all_orders_stride():
+    modes = zb.full_mode_set(14)
+    M, P = len(modes), 3000
+    ctx, plan = _plan(modes)
+    grid = zb.linear_radial_grid(P)
+    ld, ostride = P + 2, (P + 2) * M + 64
+    out = torch.zeros(4 * ostride, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib.zk_radial_eval(ctx.handle, plan.handle, grid.ctypes.data, P, 3, 1,
+                                       out.data_ptr(), ld, ostride, _lib.ZK_HOST_INPUT), "radial")
+    host = out.cpu().numpy()
+    for k in range(4):
+        blk = host[k * ostride:k * ostride + ld * M].reshape(M, ld).T[:P]
+        assert np.array_equal(blk, radial(modes, grid, k)), k
+
+
+def test_multi_chunk_host_pipeline_matches_device():
+    modes = zb.full_mode_set(100)  # 5151 columns -> ~6.5k points per 256 MB chunk
+    P = 40_001
+    grid = np.random.default_rng(4).uniform(size=P)
+    host = radial(modes, grid, 0)  # chunked D2H path
+    ctx, plan = _plan(modes)
+    d_rho = torch.tensor(grid, device="cuda")
+    out = torch.empty((len(modes), P), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib.zk_radial_eval(ctx.handle, plan.handle, d_rho.data_ptr(), P, 0, 0,
+                                       out.data_ptr(), P, 0, 0), "radial")
+    assert np.array_equal(out.cpu().numpy().T, host)
+
+
+def test_launch_counter_and_errors():
+    modes = zb.full_mode_set(4)
+    ctx, plan = _plan(modes)
+    before = ctx.launches()
+    radial(modes, [0.1, 0.2], 1)
+    assert ctx.launches() > before
+    d = torch.zeros(16, dtype=torch.float64, device="cuda")
+    rc = _lib.lib.zk_radial_eval(ctx.handle, plan.handle, d.data_ptr(), 2, 4, 0, d.data_ptr(), 2,
+                                 0, 0)
+    assert rc == _lib.ZK_EINVAL
+    rc = _lib.lib.zk_radial_eval(ctx.handle, plan.handle, d.data_ptr(), 4, 0, 0, d.data_ptr(), 2,
+                                 0, 0)
+    assert rc == _lib.ZK_EINVAL  # ld < P
+    cnt = ctypes.c_int(0)
+    assert _lib.lib.zk_device_count(ctypes.byref(cnt)) == 0 and cnt.value >= 1
