@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -84,36 +85,72 @@ int ensure_scratch(zk_ctx* ctx, int slot, size_t bytes) {
 }
 
 struct Geometry {
-  int vec, ntiles, nchunks, tiles_per_chunk, grid;
+  int vec, ntiles, nchunks, tiles_per_chunk, grid, col_cap, stage_slots;
+  bool tma;
   size_t smem;
 };
 
-Geometry geometry(const zk_ctx* ctx, const zk_plan* plan, int64_t P, int K, bool vec2) {
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+Geometry geometry(const zk_ctx* ctx, const zk_plan* plan, int64_t P, int K, bool all, int vec,
+                  bool tma) {
   Geometry g{};
-  g.vec = vec2 ? 2 : 1;
+  g.vec = vec;
   const int64_t tile_pts = int64_t(zk::kRadialThreads) * g.vec;
   g.ntiles = static_cast<int>((P + tile_pts - 1) / tile_pts);
   const int64_t G = static_cast<int64_t>(plan->host.groups.size());
-  const int64_t target = int64_t(ctx->sm_count) * 32;  // ~several resident waves
+  const int64_t target = int64_t(ctx->sm_count) * env_int("ZK_CTAS_PER_SM", 32);
   int64_t tpc = (int64_t(g.ntiles) * G + target - 1) / target;
   tpc = std::max<int64_t>(1, std::min<int64_t>(tpc, g.ntiles));
   g.tiles_per_chunk = static_cast<int>(tpc);
   g.nchunks = static_cast<int>((g.ntiles + tpc - 1) / tpc);
   g.grid = static_cast<int>(G * g.nchunks);
-  g.smem = zk::radial_smem_bytes(K, plan->host.max_jmax);
+  const int NO = all ? K + 1 : 1;
+  g.stage_slots = std::max(1, std::min(8, plan->host.max_row_cols * NO));
+  // TMA staging only pays when there is at least one full tile
+  g.tma = tma && P >= tile_pts;
+  // stage column byte offsets in smem unless one group serves very many columns
+  g.col_cap = plan->host.max_group_cols;
+  auto smem_for = [&]() {
+    return zk::radial_smem_bytes(K, all, g.vec, g.tma, g.stage_slots, plan->host.max_jmax,
+                                 g.col_cap);
+  };
+  g.smem = smem_for();
+  if (g.smem > ctx->max_smem) {
+    g.col_cap = 0;
+    g.smem = smem_for();
+  }
+  if (g.smem > ctx->max_smem && g.tma) {
+    g.tma = false;
+    g.smem = smem_for();
+  }
   return g;
 }
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // One device-resident launch of K1/K2 over P points.
 int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const double* theta,
                   int64_t P, int K, bool all, double* out, int64_t ld, int64_t ostride,
                   bool force_scalar, cudaStream_t st) {
   if (P == 0 || plan->host.groups.empty()) return ZK_OK;
-  const bool vec2 = !force_scalar && (ld % 2 == 0) && aligned16(out) &&
-                    (!all || ostride % 2 == 0);
-  Geometry geo = geometry(ctx, plan, P, K, vec2);
+  auto fits = [&](int v) {
+    return (ld % v == 0) && (reinterpret_cast<uintptr_t>(out) % (8 * v) == 0) &&
+           (!all || ostride % v == 0);
+  };
+  int vec = 1;
+  if (!force_scalar) {
+    const int want = env_int("ZK_VEC", K == 0 ? 4 : 2);
+    for (int v : {4, 2}) {
+      if (v <= want && fits(v)) {
+        vec = v;
+        break;
+      }
+    }
+  }
+  const bool tma = !force_scalar && vec >= 2 && env_int("ZK_TMA", 0) != 0;
+  Geometry geo = geometry(ctx, plan, P, K, all, vec, tma);
   if (geo.smem > ctx->max_smem)
     return fail(ZK_EINVAL, "mode set too large for the shared-memory coefficient stage "
                            "(highest jacobi degree " + std::to_string(plan->host.max_jmax) + ")");
@@ -133,7 +170,10 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
   a.ntiles = geo.ntiles;
   a.nchunks = geo.nchunks;
   a.tiles_per_chunk = geo.tiles_per_chunk;
-  cudaError_t e = zk::launch_radial(a, K, all, theta != nullptr, geo.vec, geo.grid, geo.smem, st);
+  a.col_cap = geo.col_cap;
+  a.stage_slots = geo.stage_slots;
+  a.tma_cta = env_int("ZK_TMA_CTA", 1);
+  cudaError_t e = zk::launch_radial(a, K, all, theta != nullptr, geo.vec, geo.tma, geo.grid, geo.smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "radial kernel launch");
   ctx->launches += 1;
   return ZK_OK;
@@ -192,8 +232,8 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
   const size_t budget = size_t(256) << 20;  // bytes of basis per slot
   const size_t per_point = size_t(8) * size_t(M) * NO;
   int64_t pc = static_cast<int64_t>(budget / per_point);
-  pc = std::max<int64_t>(256, pc / 256 * 256);
-  pc = std::min<int64_t>(pc, (P + 255) / 256 * 256);
+  pc = std::max<int64_t>(1024, pc / 1024 * 1024);  // whole TMA tiles per chunk
+  pc = std::min<int64_t>(pc, (P + 1023) / 1024 * 1024);
   const size_t basis_bytes = align_up(size_t(pc) * per_point, 256);
   const size_t in_bytes = align_up(size_t(pc) * 8, 256);
   for (int s = 0; s < 2; ++s) {

@@ -51,6 +51,8 @@ struct HostPlan {
   int32_t max_n = 0;
   int32_t max_order = 0;
   int32_t max_jmax = 0;
+  int32_t max_group_cols = 0;  // most columns served by one alpha group
+  int32_t max_row_cols = 0;    // most columns served by one (alpha, j) key
   std::vector<int32_t> key_n, key_m;  // unique keys, first-appearance order
   std::vector<int32_t> scatter;       // column -> key slot
   std::vector<GroupRec> groups;       // sorted by alpha

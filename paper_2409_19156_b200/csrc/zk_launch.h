@@ -9,7 +9,7 @@
 
 namespace zk {
 
-constexpr int kRadialThreads = 128;
+constexpr int kRadialThreads = 256;
 
 struct RadialArgs {
   const GroupRec* groups;
@@ -27,11 +27,16 @@ struct RadialArgs {
   int ntiles;             // ceil(P / (threads*VEC))
   int nchunks;            // CTAs per group
   int tiles_per_chunk;
+  int col_cap;            // column offsets staged in smem when a group has <= col_cap
+  int stage_slots;        // (column, order) slots per TMA staging stage
+  int tma_cta;            // 1: CTA-wide staging (one bulk copy per tile column), 0: per warp
 };
 
-size_t radial_smem_bytes(int K, int max_jmax);
-cudaError_t launch_radial(const RadialArgs& a, int K, bool all, bool ang, int vec, int grid,
-                          size_t smem, cudaStream_t st);
+int radial_stages(bool all);
+size_t radial_smem_bytes(int K, bool all, int vec, bool tma, int stage_slots, int max_jmax,
+                         int col_cap);
+cudaError_t launch_radial(const RadialArgs& a, int K, bool all, bool ang, int vec, bool tma,
+                          int grid, size_t smem, cudaStream_t st);
 
 struct SeriesArgs {
   const GroupRec* groups;

@@ -146,10 +146,12 @@ std::string build_plan(const int32_t* n, const int32_t* m, int64_t M, int max_or
       P.rowptr.push_back(static_cast<int32_t>(acc));
       row_start[static_cast<size_t>(row)] = acc;
       acc += count[static_cast<size_t>(row)];
+      P.max_row_cols = std::max(P.max_row_cols, count[static_cast<size_t>(row)]);
       nc += count[static_cast<size_t>(row)];
     }
     P.rowptr.push_back(static_cast<int32_t>(acc));
     P.groups[g].ncols = nc;
+    P.max_group_cols = std::max(P.max_group_cols, nc);
   }
   P.cols.assign(static_cast<size_t>(M), 0);
   std::vector<int64_t> fill = row_start;
