@@ -44,6 +44,17 @@ from .modes import (
     full_mode_set,
     make_mode,
 )
+from .series import (
+    allreduce_normal_equations,
+    fit,
+    fit_sharded,
+    gram,
+    gram_device,
+    series_device,
+    series_eval,
+    solve_normal,
+)
+from .sharding import radial_basis_shard, shard_range
 from .tables import (
     EvalMatrix,
     GridError,
@@ -64,4 +75,6 @@ __all__ = [
     "jacobi_argument", "jacobi_chain", "jacobi_derivative_scale", "jacobi_recursion_steps",
     "linear_radial_grid", "make_mode", "radial_at_zero", "radial_grid", "radial_jacobi",
     "rational_radial_grid", "zernike_basis", "zernike_eval", "zernike_radial",
+    "series_eval", "series_device", "gram", "gram_device", "fit", "fit_sharded",
+    "solve_normal", "allreduce_normal_equations", "shard_range", "radial_basis_shard",
 ]

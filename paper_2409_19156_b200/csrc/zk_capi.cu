@@ -481,14 +481,174 @@ int zk_zernike_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const d
                      order_stride, flags);
 }
 
-int zk_series_eval(zk_ctx*, const zk_plan*, const double*, const double*, int64_t, int,
-                   const double*, int64_t, int64_t, double*, int64_t, uint32_t) {
-  return fail(ZK_EINVAL, "zk_series_eval: not available in this build");
+int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const double* theta,
+                   int64_t P, int deriv_order, const double* coef, int64_t ncoef, int64_t ldc,
+                   double* f, int64_t ldf, uint32_t flags) {
+  if (!ctx || !plan) return fail(ZK_EINVAL, "null ctx or plan");
+  if (plan->ctx != ctx) return fail(ZK_EINVAL, "plan belongs to another context");
+  if (deriv_order < 0 || deriv_order > plan->host.max_order)
+    return fail(ZK_EINVAL, "derivative order must be 0..3, got " + std::to_string(deriv_order));
+  const int64_t M = plan->host.M;
+  if (P < 0 || ncoef < 0) return fail(ZK_EINVAL, "negative size");
+  if (P == 0 || ncoef == 0) return ZK_OK;
+  if (!rho || !f || (M > 0 && !coef)) return fail(ZK_EINVAL, "null data pointer");
+  if (ldc < M || ldf < P) return fail(ZK_EINVAL, "ldc must be >= M and ldf >= P");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  ZK_CUDA(cudaSetDevice(ctx->device));
+  const bool host_in = (flags & ZK_HOST_INPUT) != 0;
+  const bool host_out = (flags & ZK_HOST_OUTPUT) != 0;
+  cudaStream_t st = ctx->stream;
+  const size_t pb = align_up(size_t(P) * 8, 256);
+  const size_t cb = align_up(size_t(std::max<int64_t>(M, 1)) * ncoef * 8, 256);
+  const size_t fb = align_up(size_t(P) * ncoef * 8, 256);
+  int rc = ensure_scratch(ctx, 0, (host_in ? 2 * pb + cb : 0) + (host_out ? fb : 0) + 256);
+  if (rc) return rc;
+  char* base = static_cast<char*>(ctx->scratch[0]);
+  const double* d_rho = rho;
+  const double* d_theta = theta;
+  const double* d_coef = coef;
+  int64_t d_ldc = ldc;
+  if (host_in) {
+    double* r = reinterpret_cast<double*>(base);
+    ZK_CUDA(cudaMemcpyAsync(r, rho, size_t(P) * 8, cudaMemcpyHostToDevice, st));
+    d_rho = r;
+    if (theta) {
+      double* t = reinterpret_cast<double*>(base + pb);
+      ZK_CUDA(cudaMemcpyAsync(t, theta, size_t(P) * 8, cudaMemcpyHostToDevice, st));
+      d_theta = t;
+    }
+    if (M > 0) {
+      double* cc = reinterpret_cast<double*>(base + 2 * pb);
+      ZK_CUDA(cudaMemcpy2DAsync(cc, size_t(M) * 8, coef, size_t(ldc) * 8, size_t(M) * 8,
+                                size_t(ncoef), cudaMemcpyHostToDevice, st));
+      d_coef = cc;
+      d_ldc = M;
+    }
+    base += 2 * pb + cb;
+  }
+  double* d_f = f;
+  int64_t d_ldf = ldf;
+  if (host_out) {
+    d_f = reinterpret_cast<double*>(base);
+    d_ldf = P;
+  }
+  if (M == 0 || plan->host.groups.empty()) {
+    ZK_CUDA(cudaMemset2DAsync(d_f, size_t(d_ldf) * 8, 0, size_t(P) * 8, size_t(ncoef), st));
+  } else {
+    zk::SeriesArgs a{};
+    a.groups = plan->groups;
+    a.ngroups = static_cast<int>(plan->host.groups.size());
+    a.rowptr = plan->rowptr;
+    a.cols = plan->cols;
+    a.coef = plan->coef;
+    a.asmc = plan->asmc;
+    a.rho = d_rho;
+    a.theta = d_theta;
+    a.c = d_coef;
+    a.ldc = d_ldc;
+    a.ncoef = static_cast<int>(ncoef);
+    a.f = d_f;
+    a.ldf = d_ldf;
+    a.P = P;
+    int launches = 0;
+    cudaError_t e = zk::launch_series(a, plan->order, deriv_order, st, &launches);
+    ctx->launches += launches;
+    if (e != cudaSuccess) return cuda_fail(e, "series kernel launch");
+  }
+  if (host_out)
+    ZK_CUDA(cudaMemcpy2DAsync(f, size_t(ldf) * 8, d_f, size_t(P) * 8, size_t(P) * 8,
+                              size_t(ncoef), cudaMemcpyDeviceToHost, st));
+  if (!(flags & ZK_ASYNC) || host_in || host_out) ZK_CUDA(cudaStreamSynchronize(st));
+  return ZK_OK;
 }
 
-int zk_gram_accumulate(zk_ctx*, const zk_plan*, const double*, const double*, int64_t,
-                       const double*, double*, double*, uint32_t) {
-  return fail(ZK_EINVAL, "zk_gram_accumulate: not available in this build");
+int zk_gram_accumulate(zk_ctx* ctx, const zk_plan* plan, const double* rho, const double* theta,
+                       int64_t P, const double* y, double* G, double* Bty, uint32_t flags) {
+  if (!ctx || !plan) return fail(ZK_EINVAL, "null ctx or plan");
+  if (plan->ctx != ctx) return fail(ZK_EINVAL, "plan belongs to another context");
+  const int64_t M = plan->host.M;
+  if (P < 0) return fail(ZK_EINVAL, "negative point count");
+  if (P == 0 || M == 0) return ZK_OK;
+  if (!rho || !G || (y && !Bty)) return fail(ZK_EINVAL, "null data pointer");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  ZK_CUDA(cudaSetDevice(ctx->device));
+  const bool host_in = (flags & ZK_HOST_INPUT) != 0;
+  const bool host_out = (flags & ZK_HOST_OUTPUT) != 0;
+  const bool ang = theta != nullptr;
+  cudaStream_t st = ctx->stream;
+
+  // panel geometry: [B | y | 0-pad] is Pp points x Mp columns, Mp = 128-multiple
+  const int64_t BMg = 128;
+  const int64_t Mp = (M + 1 + BMg - 1) / BMg * BMg;
+  const int64_t nb = Mp / BMg;
+  const int64_t ntri = nb * (nb + 1) / 2;
+  const int64_t budget = int64_t(env_int("ZK_GRAM_PANEL_MB", 2048)) << 20;
+  int64_t Pp = budget / (Mp * 8) / 1024 * 1024;
+  Pp = std::max<int64_t>(1024, std::min<int64_t>(Pp, (P + 1023) / 1024 * 1024));
+  // point slices per panel: >= 2 waves of one 256-thread CTA per SM
+  int64_t ksplit = (2 * int64_t(ctx->sm_count) + ntri - 1) / ntri;
+  ksplit = std::max<int64_t>(1, std::min<int64_t>(ksplit, Pp / (16 * 32)));
+  const size_t panel_b = align_up(size_t(Pp) * size_t(Mp) * 8, 256);
+  const size_t part_b = align_up(size_t(ksplit) * ntri * BMg * BMg * 8, 256);
+  const size_t in_b = align_up(size_t(Pp) * 8, 256);
+  const size_t g_b = align_up(size_t(M) * M * 8, 256);
+  const size_t acc_b = host_out ? g_b + align_up(size_t(M) * 8, 256) : 0;
+  int rc = ensure_scratch(ctx, 0, panel_b + part_b + 3 * in_b + acc_b + 256);
+  if (rc) return rc;
+  char* base = static_cast<char*>(ctx->scratch[0]);
+  double* panel = reinterpret_cast<double*>(base);
+  double* part = reinterpret_cast<double*>(base + panel_b);
+  double* s_rho = reinterpret_cast<double*>(base + panel_b + part_b);
+  double* s_th = s_rho + in_b / 8;
+  double* s_y = s_th + in_b / 8;
+  double* dG = G;
+  double* dB = y ? Bty : nullptr;
+  if (host_out) {
+    dG = reinterpret_cast<double*>(base + panel_b + part_b + 3 * in_b);
+    dB = y ? dG + g_b / 8 : nullptr;
+    ZK_CUDA(cudaMemcpyAsync(dG, G, size_t(M) * M * 8, cudaMemcpyHostToDevice, st));
+    if (y) ZK_CUDA(cudaMemcpyAsync(dB, Bty, size_t(M) * 8, cudaMemcpyHostToDevice, st));
+  }
+  // zero padding columns (M+1 .. Mp-1) and, if y is absent, the y column
+  ZK_CUDA(cudaMemsetAsync(panel, 0, panel_b, st));
+  for (int64_t p0 = 0; p0 < P; p0 += Pp) {
+    const int64_t n = std::min<int64_t>(Pp, P - p0);
+    if (n < Pp && p0 > 0)  // rows past a partial last panel still hold the previous panel
+      ZK_CUDA(cudaMemset2DAsync(panel + n, size_t(Pp) * 8, 0, size_t(Pp - n) * 8,
+                                size_t(M + 1), st));
+    const double* r_in = rho + p0;
+    const double* t_in = ang ? theta + p0 : nullptr;
+    if (host_in) {
+      ZK_CUDA(cudaMemcpyAsync(s_rho, rho + p0, size_t(n) * 8, cudaMemcpyHostToDevice, st));
+      r_in = s_rho;
+      if (ang) {
+        ZK_CUDA(cudaMemcpyAsync(s_th, theta + p0, size_t(n) * 8, cudaMemcpyHostToDevice, st));
+        t_in = s_th;
+      }
+    }
+    rc = launch_device(ctx, plan, r_in, t_in, n, 0, false, panel, Pp, 0, false, st);
+    if (rc) return rc;
+    if (y) {
+      if (host_in) {
+        ZK_CUDA(cudaMemcpyAsync(s_y, y + p0, size_t(n) * 8, cudaMemcpyHostToDevice, st));
+        ZK_CUDA(cudaMemcpyAsync(panel + M * Pp, s_y, size_t(n) * 8, cudaMemcpyDeviceToDevice, st));
+      } else {
+        ZK_CUDA(cudaMemcpyAsync(panel + M * Pp, y + p0, size_t(n) * 8, cudaMemcpyDeviceToDevice,
+                                st));
+      }
+    }
+    int launches = 0;
+    cudaError_t e = zk::launch_gram_panel(panel, Pp, Pp, M, static_cast<int>(ksplit), part, dG,
+                                          dB, st, &launches);
+    ctx->launches += launches;
+    if (e != cudaSuccess) return cuda_fail(e, "gram kernel launch");
+  }
+  if (host_out) {
+    ZK_CUDA(cudaMemcpyAsync(G, dG, size_t(M) * M * 8, cudaMemcpyDeviceToHost, st));
+    if (y) ZK_CUDA(cudaMemcpyAsync(Bty, dB, size_t(M) * 8, cudaMemcpyDeviceToHost, st));
+  }
+  if (!(flags & ZK_ASYNC) || host_in || host_out) ZK_CUDA(cudaStreamSynchronize(st));
+  return ZK_OK;
 }
 
 int zk_jacobi_chain(zk_ctx* ctx, const double* x, int64_t N, int j_max, int alpha, int beta,

@@ -1,0 +1,191 @@
+// K4: least-squares normal equations on fp64 tensor cores.
+//
+// G += B^T B and Bty += B^T y over P points, B the (2-D or radial) basis.
+// Points stream through panels: K1/K2 writes the panel [B | y] (Pp x Mp,
+// column-major, y as column M, zero padding to a multiple of 128 columns),
+// then a DMMA SYRK computes the upper-triangle 128x128 blocks of
+// [B y]^T [B y] -- whose column M is B^T y -- split over point slices, and a
+// fixed-order reduction adds the slices into G (mirrored) and Bty. Every sum
+// has a fixed order, so the result is deterministic run to run.
+//
+// Tensor cores: mma.sync.m16n8k4.f64 (SASS DMMA.8x8x4). tcgen05.mma has no
+// f64 kind on sm_100a, so warp-level DMMA is the fp64 tensor path; measured
+// peak 36.9 TFLOP/s on B200 (tools/fp64_peak_probe.cu), equal to DFMA.
+// Operands are staged with cp.async (16-byte, L2-only) in a 3-stage ring.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "zk_launch.h"
+
+namespace zk {
+
+namespace {
+constexpr int BM = 128;       // G block edge
+constexpr int BK = 16;        // points per pipeline stage
+constexpr int LDS = BK + 4;   // padded smem row (doubles): conflict-free fragments
+constexpr int STAGES = 3;
+constexpr int THREADS = 256;  // 8 warps: 2 (rows) x 4 (cols), warp tile 64 x 32
+constexpr int TILE_DBL = BM * LDS;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+
+__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+__device__ __forceinline__ void tri_block(int t, int nb, int& bi, int& bj) {
+  int row = 0;
+  while (t >= nb - row) {
+    t -= nb - row;
+    ++row;
+  }
+  bi = row;
+  bj = row + t;
+}
+}  // namespace
+
+// partial[ks][blk] = sum over the slice's points of panel[:, I]^T panel[:, J]
+__global__ void __launch_bounds__(THREADS, 1)
+syrk_partial_kernel(const double* __restrict__ panel, long long ld, int nb, int ntri,
+                    long long kslice, long long kpanel, double* __restrict__ part) {
+  extern __shared__ __align__(16) double smem[];
+  const int blk = blockIdx.x % ntri;
+  const int ks = blockIdx.x / ntri;
+  int bi, bj;
+  tri_block(blk, nb, bi, bj);
+  const bool diag = bi == bj;
+  const long long k0 = ks * kslice;
+  const long long k1 = min(kpanel, k0 + kslice);
+  const int nk = k0 < k1 ? static_cast<int>((k1 - k0) / BK) : 0;
+  const double* colA = panel + static_cast<long long>(bi) * BM * ld;
+  const double* colB = panel + static_cast<long long>(bj) * BM * ld;
+  double* sA = smem;
+  double* sB = smem + STAGES * TILE_DBL;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+
+  auto load_stage = [&](int stage, int kt) {
+    const long long kb = k0 + static_cast<long long>(kt) * BK;
+#pragma unroll
+    for (int it = 0; it < (BM * BK / 2) / THREADS; ++it) {  // 16-byte chunks
+      const int idx = it * THREADS + tid;
+      const int col = idx >> 3, ch = idx & 7;
+      cp_async16(sA + stage * TILE_DBL + col * LDS + ch * 2, colA + col * ld + kb + ch * 2);
+      if (!diag)
+        cp_async16(sB + stage * TILE_DBL + col * LDS + ch * 2, colB + col * ld + kb + ch * 2);
+    }
+  };
+
+  double acc[4][4][4];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[mi][ni][e] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
+    __syncthreads();
+    const int nxt = kt + STAGES - 1;
+    if (nxt < nk) load_stage(nxt % STAGES, nxt);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const double* a = sA + (kt % STAGES) * TILE_DBL + (wm * 64) * LDS;
+    const double* b = (diag ? sA : sB) + (kt % STAGES) * TILE_DBL + (wn * 32) * LDS;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4][2], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        af[mi][0] = a[(mi * 16 + g) * LDS + kk + t];
+        af[mi][1] = a[(mi * 16 + g + 8) * LDS + kk + t];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) bf[ni] = b[(ni * 8 + g) * LDS + kk + t];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+
+  double* out = part + (static_cast<long long>(ks) * ntri + blk) * BM * BM;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int r = wm * 64 + mi * 16 + g;
+      const int c = wn * 32 + ni * 8 + 2 * t;
+      *reinterpret_cast<double2*>(out + r * BM + c) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      *reinterpret_cast<double2*>(out + (r + 8) * BM + c) =
+          make_double2(acc[mi][ni][2], acc[mi][ni][3]);
+    }
+}
+
+// G[i,j] += sum_ks part (mirrored), Bty[i] += column M; fixed summation order.
+__global__ void __launch_bounds__(256)
+syrk_reduce_kernel(const double* __restrict__ part, int nb, int ntri, int ksplit, long long M,
+                   double* __restrict__ G, double* __restrict__ Bty) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<long long>(ntri) * BM * BM) return;
+  const int blk = static_cast<int>(e / (BM * BM));
+  const int rc = static_cast<int>(e - static_cast<long long>(blk) * BM * BM);
+  const int r = rc / BM, c = rc % BM;
+  int bi, bj;
+  tri_block(blk, nb, bi, bj);
+  if (bi == bj && r > c) return;  // the mirror of (c, r)
+  const long long i = static_cast<long long>(bi) * BM + r;
+  const long long j = static_cast<long long>(bj) * BM + c;
+  if (i >= M || j > M) return;
+  double s = 0.0;
+  for (int ks = 0; ks < ksplit; ++ks) s += part[(static_cast<long long>(ks) * ntri + blk) * BM * BM + rc];
+  if (j == M) {
+    if (Bty) Bty[i] += s;
+    return;
+  }
+  G[i + j * M] += s;
+  if (i != j) G[j + i * M] += s;
+}
+
+size_t gram_smem_bytes() { return size_t(2) * STAGES * TILE_DBL * sizeof(double); }
+
+cudaError_t launch_gram_panel(const double* panel, long long ld, long long kpanel, long long M,
+                              int ksplit, double* part, double* G, double* Bty, cudaStream_t st,
+                              int* launches) {
+  const int nb = static_cast<int>((M + 1 + BM - 1) / BM);
+  const int ntri = nb * (nb + 1) / 2;
+  long long kslice = (kpanel + ksplit - 1) / ksplit;
+  kslice = (kslice + BK - 1) / BK * BK;
+  const size_t smem = gram_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(syrk_partial_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  syrk_partial_kernel<<<ntri * ksplit, THREADS, smem, st>>>(panel, ld, nb, ntri, kslice, kpanel,
+                                                            part);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const long long n = static_cast<long long>(ntri) * BM * BM;
+  syrk_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(part, nb, ntri,
+                                                                             ksplit, M, G, Bty);
+  *launches += 2;
+  return cudaGetLastError();
+}
+
+}  // namespace zk

@@ -55,27 +55,13 @@ struct SeriesArgs {
   long long P;
 };
 
-cudaError_t launch_series(const SeriesArgs& a, int K, cudaStream_t st, int* launches);
+cudaError_t launch_series(const SeriesArgs& a, const int32_t* order, int K, cudaStream_t st,
+                          int* launches);
 
-struct GramArgs {
-  const GroupRec* groups;
-  int ngroups;
-  const int32_t* rowptr;
-  const int32_t* cols;
-  const ChainCoef* coef;
-  const AsmCoef* asmc;
-  const double* rho;
-  const double* theta;
-  const double* y;
-  long long P;
-  long long M;
-  double* G;
-  double* Bty;
-  double* scratch;        // basis panel, P_panel x M column-major
-  long long panel;        // points per panel
-};
-
-cudaError_t launch_gram(const GramArgs& a, cudaStream_t st, int* launches);
+size_t gram_smem_bytes();
+cudaError_t launch_gram_panel(const double* panel, long long ld, long long kpanel, long long M,
+                              int ksplit, double* part, double* G, double* Bty, cudaStream_t st,
+                              int* launches);
 
 cudaError_t launch_chain(const double* x, long long N, int jmax, int alpha, int beta,
                          double* out, long long ldo, cudaStream_t st);

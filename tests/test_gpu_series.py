@@ -1,0 +1,115 @@
+"""GPU parity of K3 (fused series f = B c), K4 (DMMA Gram B^T B, B^T y) and
+the fit (K6) against the oracle / golden vectors. Calls go through the C ABI."""
+
+import numpy as np
+import pytest
+
+import zk_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+zb = pytest.importorskip("paper_2409_19156_b200")
+torch = pytest.importorskip("torch")
+
+
+def disc(P, seed):
+    rng = np.random.default_rng(seed)
+    return np.sqrt(rng.uniform(size=P)), 2 * np.pi * rng.uniform(size=P)
+
+
+def test_series_matches_golden_config5(golden):
+    modes = zb.full_mode_set(60)
+    f = zb.series_eval(modes, golden["c5_coef"], golden["c5_rho"], golden["c5_theta"])
+    scale = np.abs(golden["c5_B"]) @ np.abs(golden["c5_coef"])
+    assert (np.abs(f - golden["c5_f"]) <= 1e-13 * scale + 1e-13).all()
+
+
+@pytest.mark.parametrize("V", [1, 3, 8, 11])
+def test_series_multi_vector_2d(V):
+    modes = zb.full_mode_set(25)
+    rho, theta = disc(777, V)
+    C = np.random.default_rng(V).standard_normal((len(modes), V))
+    f = zb.series_eval(modes, C, rho, theta)
+    B = orc.basis_2d([(md.n, md.m) for md in modes], rho, theta)
+    ref = B @ C
+    assert f.shape == (777, V)
+    assert np.abs(f - ref).max() <= 1e-12 * np.abs(B).sum(axis=1).max() * np.abs(C).max()
+
+
+@pytest.mark.parametrize("k", [0, 2, 3])
+def test_series_radial_derivatives(k):
+    modes = zb.full_mode_set(30)
+    rho = zb.linear_radial_grid(500)
+    c = np.random.default_rng(k).standard_normal(len(modes))
+    f = zb.series_eval(modes, c, rho, None, k)
+    B = orc.radial_batch([(md.n, md.m) for md in modes], rho, k)
+    scale = np.abs(B) @ np.abs(c)
+    assert (np.abs(f - B @ c) <= 1e-12 * scale + 1e-13).all()
+
+
+def test_gram_matches_numpy_and_is_symmetric():
+    modes = zb.full_mode_set(20)
+    pairs = [(md.n, md.m) for md in modes]
+    rho, theta = disc(5000, 1)
+    y = np.random.default_rng(2).standard_normal(5000)
+    G, r = zb.gram(modes, rho, theta, y)
+    B = orc.basis_2d(pairs, rho, theta)
+    Gr, rr = B.T @ B, B.T @ y
+    assert np.array_equal(G, G.T)
+    assert np.abs(G - Gr).max() <= 1e-12 * np.abs(Gr).max()
+    assert np.abs(r - rr).max() <= 1e-12 * np.abs(B).sum(axis=0).max() * np.abs(y).max()
+    G2, _ = zb.gram(modes, rho, theta, None)
+    assert np.array_equal(G2, G)  # y column does not perturb B^T B
+    G3, r3 = zb.gram(modes, rho, theta, y)
+    assert np.array_equal(G3, G) and np.array_equal(r3, r)  # deterministic
+
+
+def test_gram_multi_panel_and_partial_tail(monkeypatch):
+    modes = zb.full_mode_set(15)
+    pairs = [(md.n, md.m) for md in modes]
+    rho, theta = disc(10_000, 3)
+    y = np.random.default_rng(4).standard_normal(10_000)
+    B = orc.basis_2d(pairs, rho, theta)
+    monkeypatch.setenv("ZK_GRAM_PANEL_MB", "3")  # 3 MB / (256 cols * 8 B) -> 1024-point panels
+    G, r = zb.gram(modes, rho, theta, y)
+    assert np.abs(G - B.T @ B).max() <= 1e-12 * np.abs(B.T @ B).max()
+    assert np.abs(r - B.T @ y).max() <= 1e-11 * np.abs(B.T @ y).max()
+
+
+def test_gram_radial_basis_and_config5_shape():
+    modes = zb.full_mode_set(60)
+    pairs = [(md.n, md.m) for md in modes]
+    rho, theta = disc(20_000, 5)
+    G, _ = zb.gram(modes, rho, theta)
+    B = orc.basis_2d(pairs, rho, theta)
+    Gr = B.T @ B
+    assert G.shape == (1891, 1891)
+    assert np.abs(G - Gr).max() <= 1e-12 * np.abs(Gr).max()
+    Gr2, _ = zb.gram(modes, rho, None)
+    Br = orc.radial_batch(pairs, rho, 0)
+    assert np.abs(Gr2 - Br.T @ Br).max() <= 1e-12 * np.abs(Br.T @ Br).max()
+
+
+def test_fit_recovers_coefficients():
+    modes = zb.full_mode_set(12)
+    rho, theta = disc(20_000, 6)
+    c = np.random.default_rng(7).standard_normal(len(modes))
+    y = zb.series_eval(modes, c, rho, theta)
+    x = zb.fit(modes, rho, theta, y)
+    assert np.abs(x - c).max() < 1e-9
+
+
+def test_device_accumulate_equals_single_call():
+    modes = zb.full_mode_set(10)
+    rho, theta = disc(4096, 8)
+    y = np.random.default_rng(9).standard_normal(4096)
+    t = lambda a: torch.tensor(a, dtype=torch.float64, device="cuda")
+    G, r = zb.gram_device(modes, t(rho[:2000]), t(theta[:2000]), t(y[:2000]))
+    G, r = zb.gram_device(modes, t(rho[2000:]), t(theta[2000:]), t(y[2000:]), G, r)
+    Gh, rh = zb.gram(modes, rho, theta, y)
+    assert np.abs(G.cpu().numpy() - Gh).max() <= 1e-12 * np.abs(Gh).max()
+    assert np.abs(r.cpu().numpy() - rh).max() <= 1e-11 * np.abs(rh).max()
+    x, Gs, rs = zb.fit_sharded(modes, t(rho), t(theta), t(y))  # world of one
+    assert np.abs(x.cpu().numpy() - np.linalg.solve(Gh, rh)).max() < 1e-8
+    f = zb.series_device(modes, x, t(rho), t(theta))
+    assert f.shape == (4096,)
