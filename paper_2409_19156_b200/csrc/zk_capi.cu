@@ -102,7 +102,7 @@ Geometry geometry(const zk_ctx* ctx, const zk_plan* plan, int64_t P, int K, bool
   const int64_t tile_pts = int64_t(zk::kRadialThreads) * g.vec;
   g.ntiles = static_cast<int>((P + tile_pts - 1) / tile_pts);
   const int64_t G = static_cast<int64_t>(plan->host.groups.size());
-  const int64_t target = int64_t(ctx->sm_count) * env_int("ZK_CTAS_PER_SM", 32);
+  const int64_t target = int64_t(ctx->sm_count) * env_int("ZK_CTAS_PER_SM", 1 << 20);
   int64_t tpc = (int64_t(g.ntiles) * G + target - 1) / target;
   tpc = std::max<int64_t>(1, std::min<int64_t>(tpc, g.ntiles));
   g.tiles_per_chunk = static_cast<int>(tpc);
@@ -112,17 +112,13 @@ Geometry geometry(const zk_ctx* ctx, const zk_plan* plan, int64_t P, int K, bool
   g.stage_slots = std::max(1, std::min(8, plan->host.max_row_cols * NO));
   // TMA staging only pays when there is at least one full tile
   g.tma = tma && P >= tile_pts;
-  // stage column byte offsets in smem unless one group serves very many columns
+  // column byte offsets of the CTA's group live in smem (planner caps group size)
   g.col_cap = plan->host.max_group_cols;
   auto smem_for = [&]() {
     return zk::radial_smem_bytes(K, all, g.vec, g.tma, g.stage_slots, plan->host.max_jmax,
                                  g.col_cap);
   };
   g.smem = smem_for();
-  if (g.smem > ctx->max_smem) {
-    g.col_cap = 0;
-    g.smem = smem_for();
-  }
   if (g.smem > ctx->max_smem && g.tma) {
     g.tma = false;
     g.smem = smem_for();
@@ -172,7 +168,6 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
   a.tiles_per_chunk = geo.tiles_per_chunk;
   a.col_cap = geo.col_cap;
   a.stage_slots = geo.stage_slots;
-  a.tma_cta = env_int("ZK_TMA_CTA", 1);
   cudaError_t e = zk::launch_radial(a, K, all, theta != nullptr, geo.vec, geo.tma, geo.grid, geo.smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "radial kernel launch");
   ctx->launches += 1;

@@ -46,6 +46,10 @@ struct GroupRec {
 };
 static_assert(sizeof(GroupRec) == 32, "GroupRec layout");
 
+// Most columns one alpha group (one CTA's shared-memory offset table) may serve;
+// larger groups are split into virtual groups by the planner.
+constexpr int32_t kMaxGroupCols = 4096;
+
 struct HostPlan {
   int64_t M = 0;
   int32_t max_n = 0;

@@ -29,7 +29,6 @@ struct RadialArgs {
   int tiles_per_chunk;
   int col_cap;            // column offsets staged in smem when a group has <= col_cap
   int stage_slots;        // (column, order) slots per TMA staging stage
-  int tma_cta;            // 1: CTA-wide staging (one bulk copy per tile column), 0: per warp
 };
 
 int radial_stages(bool all);

@@ -161,6 +161,46 @@ std::string build_plan(const int32_t* n, const int32_t* m, int64_t M, int max_or
         static_cast<int32_t>(c * 2 + (m[c] < 0 ? 1 : 0));
   }
 
+  // groups serving more than kMaxGroupCols columns (only possible with heavy
+  // duplication) are split into virtual groups over disjoint column subsets,
+  // so every CTA can stage its column offsets in shared memory
+  {
+    std::vector<GroupRec> ng;
+    std::vector<int32_t> nrow, ncol;
+    for (const GroupRec& g : P.groups) {
+      const int32_t nj = g.jmax + 1;
+      const int32_t* rp = P.rowptr.data() + g.row0;
+      int32_t j = 0, k = 0;  // next row and position inside it
+      do {
+        GroupRec v = g;
+        v.row0 = static_cast<int32_t>(nrow.size());
+        int32_t taken = 0;
+        for (int32_t jj = 0; jj < nj; ++jj) {
+          nrow.push_back(static_cast<int32_t>(ncol.size()));
+          if (jj != j) continue;  // only the current row can take columns
+          const int32_t row_n = rp[jj + 1] - rp[jj];
+          while (k < row_n && taken < kMaxGroupCols) {
+            ncol.push_back(P.cols[static_cast<size_t>(rp[jj] + k)]);
+            ++k;
+            ++taken;
+          }
+          if (k == row_n) {
+            ++j;
+            k = 0;
+          }
+        }
+        nrow.push_back(static_cast<int32_t>(ncol.size()));
+        v.ncols = taken;
+        ng.push_back(v);
+      } while (j < nj);
+    }
+    P.groups.swap(ng);
+    P.rowptr.swap(nrow);
+    P.cols.swap(ncol);
+    P.max_group_cols = 0;
+    for (const GroupRec& g : P.groups) P.max_group_cols = std::max(P.max_group_cols, g.ncols);
+  }
+
   // exact recursion coefficients, chains i = 0..max_order (alpha+i, beta=i)
   for (auto& g : P.groups) {
     g.coef_off = static_cast<int32_t>(P.coef.size());

@@ -8,29 +8,36 @@
 // degree j is written as soon as its value exists -- the reference's
 // unique->scatter gather (zk/batch.py:97-101) happens in the store address.
 //
-// Store path (the roofline: 8 bytes per eval vs ~10 fp64 ops per unique key,
-// SURVEY §8d). The output is column-major ("point-fastest", ld >= P), so one
-// column of one tile is TILE*8 contiguous bytes (8 KB for k=0). Values are
-// staged in shared memory -- one slot per (warp, column, order) -- and each
-// slot leaves as ONE TMA bulk copy (cp.async.bulk.global.shared::cta, SASS
-// UBLKCP) of the warp's 32*VEC points: whole 128-byte lines, issued by lane 0,
-// asynchronous to the recursion. Each warp runs its own ring of S stages with
-// only __syncwarp between writing a stage and shipping it, so warps never wait
-// on each other and the copies overlap the next degree's arithmetic. Measured on B200
-// (tools/pattern_probe.cu): this store pattern reaches cudaMemset speed
-// (~7.3 TB/s), per-thread 16/32-byte stores of the same layout ~6.5-6.9 TB/s.
-// Partial tiles and layouts TMA cannot address (odd ld, unaligned out) use
-// direct vector stores.
+// Store paths (the roofline is the HBM write stream: 8 bytes per eval vs ~10
+// fp64 ops per unique key). The output is column-major
+// ("point-fastest", ld >= P): one column of one tile is TP*8 contiguous bytes.
+//  * direct (TMA=false): each thread stores its VEC values of a column with
+//    one 32-byte st.global.v4.f64 (SASS STG.E.ENL2.256) -- a warp covers 1 KB.
+//  * TMA ring (TMA=true): the 8 compute warps write every (column, order)
+//    slot of the tile into a shared-memory stage; a dedicated producer warp
+//    ships each slot with ONE bulk copy (cp.async.bulk.global.shared::cta,
+//    SASS UBLKCP) of TP*8 contiguous bytes. Stages are handed over through
+//    mbarriers (full: 8 warp arrivals; empty: released by the producer once
+//    the bulk copy has read the stage), so compute warps never wait for each
+//    other -- only when the ring is full. Partial tiles use direct stores.
 //
 // Per CTA, the group's integer recursion coefficients, derivative prefactors
 // and the byte offsets of its columns (col*ld*8, |m|-sign in bit 0) are
 // staged once in shared memory and read as warp-uniform broadcasts.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "zk_kernels.cuh"
 #include "zk_launch.h"
 
 namespace zk {
+
+namespace {
+
+constexpr int kComputeWarps = kRadialThreads / 32;
+constexpr int kRingStages = 4;  // TMA staging ring depth
+constexpr int kRingLag = 1;     // bulk groups the producer keeps in flight before releasing
 
 template <int VEC>
 __device__ __forceinline__ void store_vec(double* dst, const double (&w)[VEC]) {
@@ -57,12 +64,38 @@ __device__ __forceinline__ void store_smem(double* dst, const double (&w)[VEC]) 
   }
 }
 
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(ssrc));
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s),
-               "r"(bytes)
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_addr(ssrc)), "r"(bytes)
                : "memory");
 }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+}  // namespace
 
 template <int K, bool ALL, bool ANG, int VEC>
 struct Thread {
@@ -72,14 +105,18 @@ struct Thread {
   PowSet<K> pw[VEC];
   double cur[K + 1][VEC], prev[K + 1][VEC];
 
-  // value(s) of degree j from the current chain state, (-1)^j applied
-  __device__ __forceinline__ void values(int j, const AsmCoef& ac, double (&val)[NO][VEC]) const {
+  // value(s) of degree j from chain values ch (ch[i] = P_{j-i}), (-1)^j applied.
+  // STEADY: every chain is at degree >= 2 (j >= K+2), no zero chains.
+  template <bool STEADY>
+  __device__ __forceinline__ void values(int j, const AsmCoef& ac,
+                                         const double (&chs)[K + 1][VEC],
+                                         double (&val)[NO][VEC]) const {
     const bool odd = (j & 1) != 0;
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       double ch[K + 1];
 #pragma unroll
-      for (int i = 0; i <= K; ++i) ch[i] = (j - i >= 0) ? cur[i][v] : 0.0;
+      for (int i = 0; i <= K; ++i) ch[i] = (STEADY || j - i >= 0) ? chs[i][v] : 0.0;
       if constexpr (ALL) {
         val[0][v] = assemble<0, K>(pw[v], ac, ch);
         if constexpr (K >= 1) val[1][v] = assemble<1, K>(pw[v], ac, ch);
@@ -93,25 +130,35 @@ struct Thread {
     }
   }
 
-  __device__ __forceinline__ void angular(bool neg_m, const double (&in)[VEC],
-                                          double (&w)[VEC]) const {
+  // the VEC values of order o for a column, with the angular factor
+  __device__ __forceinline__ void column(bool neg_m, int o, const double (&val)[NO][VEC],
+                                         double (&w)[VEC]) const {
 #pragma unroll
-    for (int v = 0; v < VEC; ++v)
-      w[v] = ANG ? __dmul_rn(in[v], neg_m ? sinv[v] : cosv[v]) : in[v];
+    for (int v = 0; v < VEC; ++v) {
+      double x = val[0][v];
+#pragma unroll
+      for (int oo = 1; oo < NO; ++oo)
+        if (oo == o) x = val[oo][v];
+      w[v] = ANG ? __dmul_rn(x, neg_m ? sinv[v] : cosv[v]) : x;
+    }
   }
 };
 
-template <int K, bool ALL>
-struct Stages {
-  static constexpr int S = ALL ? 3 : 4;  // ring depth of the TMA staging buffer
-};
+// CTAs per SM the register allocation must allow (latency hiding of the
+// dependent fp64 recursion needs >= 16 warps per SM): caps registers at 128
+// per thread for the default VEC choices (measured: a 149-register k=3
+// kernel at one CTA/SM ran 1.5x slower; a hard 85 cap spills for k=1,2).
+template <int K, bool ALL, int VEC, bool TMA>
+constexpr int min_ctas() {
+  return (TMA || (VEC == 4 && K > 0)) ? 1 : 2;
+}
 
 template <int K, bool ALL, bool ANG, int VEC, bool TMA>
-__global__ void __launch_bounds__(kRadialThreads)
+__global__ void __launch_bounds__(kRadialThreads + (TMA ? 32 : 0), (min_ctas<K, ALL, VEC, TMA>()))
 radial_basis_kernel(const RadialArgs a) {
   using T = Thread<K, ALL, ANG, VEC>;
   constexpr int NO = T::NO;
-  constexpr int S = Stages<K, ALL>::S;
+  constexpr int S = kRingStages;
   constexpr int TP = kRadialThreads * VEC;  // points per tile
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int slot = blockIdx.x / a.nchunks;
@@ -123,58 +170,89 @@ radial_basis_kernel(const RadialArgs a) {
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  constexpr int WP = 32 * VEC;  // points per warp sub-tile
+  const int nthreads = blockDim.x;
 
-  // ---- shared layout: [stage ring][coef][asm][col offsets][rowptr]
-  double* s_stage = reinterpret_cast<double*>(smem_raw);
+  // ---- shared layout: [mbarriers][stage ring][coef][asm][col offsets][rowptr]
+  unsigned long long* bar_full = reinterpret_cast<unsigned long long*>(smem_raw);
+  unsigned long long* bar_empty = bar_full + S;
+  double* s_stage = reinterpret_cast<double*>(smem_raw + 128);
   const int maxc = a.stage_slots;
   ChainCoef* s_coef = reinterpret_cast<ChainCoef*>(s_stage + (TMA ? S * maxc * TP : 0));
   AsmCoef* s_asm = reinterpret_cast<AsmCoef*>(s_coef + (K + 1) * nj);
-  const bool off_in_smem = g.ncols <= a.col_cap;
   long long* s_off = reinterpret_cast<long long*>(s_asm + (K > 0 ? nj : 0));
-  int* s_row = reinterpret_cast<int*>(s_off + (off_in_smem ? g.ncols : 0));
+  int* s_row = reinterpret_cast<int*>(s_off + g.ncols);
   const int row_base = __ldg(a.rowptr + g.row0);
   {
     const double* src = reinterpret_cast<const double*>(a.coef + g.coef_off);
     double* dst = reinterpret_cast<double*>(s_coef);
     const int n_coef = (K + 1) * nj * 6;
-    for (int t = tid; t < n_coef; t += kRadialThreads) dst[t] = __ldg(src + t);
+    for (int t = tid; t < n_coef; t += nthreads) dst[t] = __ldg(src + t);
     if (K > 0) {
       const double* asrc = reinterpret_cast<const double*>(a.asmc + g.asm_off);
       double* adst = reinterpret_cast<double*>(s_asm);
-      for (int t = tid; t < nj * 8; t += kRadialThreads) adst[t] = __ldg(asrc + t);
+      for (int t = tid; t < nj * 8; t += nthreads) adst[t] = __ldg(asrc + t);
     }
-    for (int t = tid; t <= nj; t += kRadialThreads)
-      s_row[t] = __ldg(a.rowptr + g.row0 + t) - row_base;
-    if (off_in_smem) {
-      for (int t = tid; t < g.ncols; t += kRadialThreads) {
-        const int code = __ldg(a.cols + row_base + t);
-        s_off[t] = (static_cast<long long>(code >> 1) * a.ld * 8) | (code & 1);
+    for (int t = tid; t <= nj; t += nthreads) s_row[t] = __ldg(a.rowptr + g.row0 + t) - row_base;
+    // byte offset of each column; bit 0 = (m < 0), only kept for the 2-D basis
+    for (int t = tid; t < g.ncols; t += nthreads) {
+      const int code = __ldg(a.cols + row_base + t);
+      s_off[t] = (static_cast<long long>(code >> 1) * a.ld * 8) | (ANG ? (code & 1) : 0);
+    }
+    if (TMA && tid == 0) {
+      for (int s = 0; s < S; ++s) {
+        mbar_init(bar_full + s, kComputeWarps);
+        mbar_init(bar_empty + s, 1);
       }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
   }
   __syncthreads();
 
   const int t_begin = chunk * a.tiles_per_chunk;
   const int t_end = min(a.ntiles, t_begin + a.tiles_per_chunk);
-  const int* cols_g = a.cols + row_base;
-  int stage = 0;
-  const bool cta_mode = a.tma_cta != 0;
-  double* w_stage = s_stage + warp * (S * maxc * WP);
+  auto col_offset = [&](int r) -> long long { return s_off[r]; };
 
-  auto col_offset = [&](int r) -> long long {
-    if (off_in_smem) return s_off[r];
-    const int code = __ldg(cols_g + r);
-    return (static_cast<long long>(code >> 1) * a.ld * 8) | (code & 1);
-  };
+  // ---- producer warp (TMA only): replays the compute warps' stage sequence
+  if (TMA && warp == kComputeWarps) {
+    if (lane == 0) {
+      unsigned use = 0;
+      for (int tile = t_begin; tile < t_end; ++tile) {
+        const long long tile0 = static_cast<long long>(tile) * TP;
+        if (tile0 + TP > a.P) continue;  // partial tile: direct stores
+        char* tbase = reinterpret_cast<char*>(a.out + tile0);
+        for (int j = 0; j <= jmax; ++j) {
+          const int r_lo = s_row[j], r_hi = s_row[j + 1];
+          const int npairs = (r_hi - r_lo) * NO;
+          for (int q0 = 0; q0 < npairs; q0 += maxc) {
+            const int q1 = min(npairs, q0 + maxc);
+            const int s = use % S;
+            mbar_wait(bar_full + s, (use / S) & 1);
+            const double* sb = s_stage + s * maxc * TP;
+            for (int q = q0; q < q1; ++q) {
+              const int r = r_lo + q / NO;
+              const int o = q - (q / NO) * NO;
+              const long long off = col_offset(r) & ~1LL;
+              bulk_store(tbase + off + o * a.ostride * 8, sb + (q - q0) * TP, TP * 8);
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            if (use >= kRingLag) {
+              asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kRingLag) : "memory");
+              mbar_arrive(bar_empty + (use - kRingLag) % S);
+            }
+            ++use;
+          }
+        }
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    return;
+  }
 
+  unsigned use = 0;  // stage uses of this warp (same sequence in every warp)
   for (int tile = t_begin; tile < t_end; ++tile) {
     const long long tile0 = static_cast<long long>(tile) * TP;
     const long long p0 = tile0 + tid * VEC;
-    const long long sub0 = tile0 + warp * WP;  // this warp's sub-tile
-    // CTA mode needs the whole tile in range (CTA-uniform); warp mode its sub-tile
-    const bool use_tma = TMA && (cta_mode ? tile0 + TP <= a.P : sub0 + WP <= a.P);
-    const int SP = cta_mode ? TP : WP;  // points per staged slot
+    const bool use_tma = TMA && tile0 + TP <= a.P;  // CTA-uniform
     const bool full = p0 + VEC <= a.P;
     T th;
     {
@@ -195,75 +273,61 @@ radial_basis_kernel(const RadialArgs a) {
       }
     }
     char* obase = reinterpret_cast<char*>(a.out + p0);
-    char* wbase = reinterpret_cast<char*>(a.out + sub0);
-    char* tbase = reinterpret_cast<char*>(a.out + tile0);
+    const long long ostride_b = a.ostride * 8;
 
-    auto emit = [&](int j) {
+    auto emit = [&](int j, const double(&chs)[K + 1][VEC], auto steady) {
       const int r_lo = s_row[j];
       const int r_hi = s_row[j + 1];
       if (r_lo == r_hi) return;  // CTA-uniform
       AsmCoef ac;
       if constexpr (K > 0) ac = s_asm[j];
       double val[NO][VEC];
-      th.values(j, ac, val);
+      th.template values<decltype(steady)::value>(j, ac, chs, val);
       if (!use_tma) {
-        for (int r = r_lo; r < r_hi; ++r) {
-          const long long off = col_offset(r);
-          double* dst0 = reinterpret_cast<double*>(obase + (off & ~1LL));
+        if (full) {
+          for (int r = r_lo; r < r_hi; ++r) {
+            const long long off = s_off[r];
+            char* dst = obase + (ANG ? (off & ~1LL) : off);
 #pragma unroll
-          for (int o = 0; o < NO; ++o) {
-            double w[VEC];
-            th.angular((off & 1) != 0, val[o], w);
-            double* dst = dst0 + o * a.ostride;
-            if (full) {
-              store_vec<VEC>(dst, w);
-            } else {
+            for (int o = 0; o < NO; ++o) {
+              double w[VEC];
+              th.column(ANG && (off & 1) != 0, o, val, w);
+              store_vec<VEC>(reinterpret_cast<double*>(dst + o * ostride_b), w);
+            }
+          }
+        } else {
+          for (int r = r_lo; r < r_hi; ++r) {
+            const long long off = s_off[r];
+            double* dst = reinterpret_cast<double*>(obase + (ANG ? (off & ~1LL) : off));
+#pragma unroll
+            for (int o = 0; o < NO; ++o) {
+              double w[VEC];
+              th.column(ANG && (off & 1) != 0, o, val, w);
 #pragma unroll
               for (int v = 0; v < VEC; ++v)
-                if (p0 + v < a.P) dst[v] = w[v];
+                if (p0 + v < a.P) dst[o * a.ostride + v] = w[v];
             }
           }
         }
         return;
       }
-      // TMA paths: every (column, order) pair of the tile (CTA mode) or of the
-      // warp's sub-tile (warp mode) goes to one smem slot, which leaves as ONE
-      // bulk copy issued by a single thread. A ring of S stages; the issuing
-      // thread waits until the stage written NEXT has been read out, then one
-      // barrier (__syncthreads / __syncwarp) publishes the stage just written.
       const int npairs = (r_hi - r_lo) * NO;
       for (int q0 = 0; q0 < npairs; q0 += maxc) {
         const int q1 = min(npairs, q0 + maxc);
-        double* sb = (cta_mode ? s_stage : w_stage) + stage * maxc * SP;
+        const int s = use % S;
+        if (use >= S) mbar_wait(bar_empty + s, ((use / S) - 1) & 1);
+        double* sb = s_stage + s * maxc * TP;
         for (int q = q0; q < q1; ++q) {
           const int r = r_lo + q / NO;
           const int o = q - (q / NO) * NO;
-          const bool neg_m = (col_offset(r) & 1) != 0;
-          double in[VEC], w[VEC];
-#pragma unroll
-          for (int oo = 0; oo < NO; ++oo)
-            if (oo == o) {
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) in[v] = val[oo][v];
-            }
-          th.angular(neg_m, in, w);
-          store_smem<VEC>(sb + (q - q0) * SP + (cta_mode ? tid : lane) * VEC, w);
+          double w[VEC];
+          th.column((col_offset(r) & 1) != 0, o, val, w);
+          store_smem<VEC>(sb + (q - q0) * TP + tid * VEC, w);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const bool issuer = cta_mode ? (tid == 0) : (lane == 0);
-        if (issuer) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(S - 2) : "memory");
-        if (cta_mode) __syncthreads(); else __syncwarp();
-        if (issuer) {
-          char* gb = cta_mode ? tbase : wbase;
-          for (int q = q0; q < q1; ++q) {
-            const int r = r_lo + q / NO;
-            const int o = q - (q / NO) * NO;
-            const long long off = col_offset(r) & ~1LL;
-            bulk_store(gb + off + o * a.ostride * 8, sb + (q - q0) * SP, SP * 8);
-          }
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        stage = (stage + 1 == S) ? 0 : stage + 1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_full + s);
+        ++use;
       }
     };
 
@@ -294,26 +358,40 @@ radial_basis_kernel(const RadialArgs a) {
           }
         }
       }
-      emit(j);
+      emit(j, th.cur, std::false_type{});
     }
-    // ---- steady state: every chain is in the three-term recursion
-#pragma unroll 2
-    for (int j = K + 2; j <= jmax; ++j) {
+    // ---- steady state: every chain in the three-term recursion. Unrolled by
+    // two with the roles of the state arrays swapped (no register moves):
+    // A holds the newest degree, B the one before.
+    double(&A)[K + 1][VEC] = th.cur;
+    double(&B)[K + 1][VEC] = th.prev;
+    int j = K + 2;
+    for (; j + 1 <= jmax; j += 2) {
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
         const ChainCoef c = s_coef[i * nj + (j - i)];
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          const double nx = jacobi_step(c, th.u[v], th.cur[i][v], th.prev[i][v]);
-          th.prev[i][v] = th.cur[i][v];
-          th.cur[i][v] = nx;
-        }
+        for (int v = 0; v < VEC; ++v) B[i][v] = jacobi_step(c, th.u[v], A[i][v], B[i][v]);
       }
-      emit(j);
+      emit(j, B, std::true_type{});
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        const ChainCoef c = s_coef[i * nj + (j + 1 - i)];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) A[i][v] = jacobi_step(c, th.u[v], B[i][v], A[i][v]);
+      }
+      emit(j + 1, A, std::true_type{});
+    }
+    if (j <= jmax) {
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        const ChainCoef c = s_coef[i * nj + (j - i)];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) B[i][v] = jacobi_step(c, th.u[v], A[i][v], B[i][v]);
+      }
+      emit(j, B, std::true_type{});
     }
   }
-  if (TMA && (cta_mode ? tid == 0 : lane == 0))
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -328,7 +406,7 @@ static cudaError_t launch_t(const RadialArgs& a, int grid, size_t smem, cudaStre
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  fn<<<grid, kRadialThreads, smem, st>>>(a);
+  fn<<<grid, kRadialThreads + (TMA ? 32 : 0), smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -360,15 +438,15 @@ static cudaError_t launch_k(const RadialArgs& a, bool all, bool ang, int vec, bo
              : launch_v<K, false, false>(a, vec, tma, grid, smem, st);
 }
 
-int radial_stages(bool all) { return all ? 3 : 4; }
+int radial_stages(bool) { return kRingStages; }
 
 size_t radial_smem_bytes(int K, bool all, int vec, bool tma, int stage_slots, int max_jmax,
                          int col_cap) {
+  (void)all;
   const size_t nj = static_cast<size_t>(max_jmax) + 1;
-  const size_t stage = tma ? size_t(radial_stages(all && K > 0)) * stage_slots *
-                                 kRadialThreads * vec * sizeof(double)
-                           : 0;
-  return stage + (K + 1) * nj * sizeof(ChainCoef) + (K > 0 ? nj * sizeof(AsmCoef) : 0) +
+  const size_t stage =
+      tma ? size_t(kRingStages) * stage_slots * kRadialThreads * vec * sizeof(double) : 0;
+  return 128 + stage + (K + 1) * nj * sizeof(ChainCoef) + (K > 0 ? nj * sizeof(AsmCoef) : 0) +
          static_cast<size_t>(col_cap) * sizeof(long long) + (nj + 1) * sizeof(int);
 }
 

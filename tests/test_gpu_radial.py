@@ -329,3 +329,18 @@ def test_launch_counter_and_errors():
     assert rc == _lib.ZK_EINVAL  # ld < P
     cnt = ctypes.c_int(0)
     assert _lib.lib.zk_device_count(ctypes.byref(cnt)) == 0 and cnt.value >= 1
+
+
+def test_heavily_duplicated_group_is_split():
+    # > 4096 columns with the same |m|: the planner splits the alpha group into
+    # virtual groups (shared-memory offset tables stay bounded)
+    pairs = [(2, 0)] * 5000 + [(6, 2), (6, -2)] * 1500 + [(4, 0)] * 300
+    modes = zb.as_mode_set(pairs)
+    grid = np.random.default_rng(11).uniform(size=300)
+    ctx, plan = _plan(modes)
+    info = plan.info()
+    assert info["U"] == 3 and info["groups"] >= 3
+    got = radial(modes, grid, 1)
+    ref = orc.radial_batch(pairs, grid, 1)
+    assert within_tolerance(got, ref)
+    assert np.array_equal(got[:, 0], got[:, 4999])
