@@ -144,18 +144,8 @@ struct Thread {
   }
 };
 
-// CTAs per SM the register allocation must allow (latency hiding of the
-// dependent fp64 recursion needs >= 16 warps per SM): caps registers at 128
-// per thread for the default VEC choices (measured: a 149-register k=3
-// kernel at one CTA/SM ran 1.5x slower; a hard 85 cap spills for k=1,2).
-template <int K, bool ALL, int VEC, bool TMA>
-constexpr int min_ctas() {
-  return (TMA || (VEC == 4 && K > 0)) ? 1 : 2;
-}
-
 template <int K, bool ALL, bool ANG, int VEC, bool TMA>
-__global__ void __launch_bounds__(kRadialThreads + (TMA ? 32 : 0), (min_ctas<K, ALL, VEC, TMA>()))
-radial_basis_kernel(const RadialArgs a) {
+__device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
   using T = Thread<K, ALL, ANG, VEC>;
   constexpr int NO = T::NO;
   constexpr int S = kRingStages;
@@ -394,13 +384,31 @@ radial_basis_kernel(const RadialArgs a) {
   }
 }
 
+// Register budgets: the compiler's default heuristic (launch bound without a
+// CTA minimum) lands at 64-80 registers for k <= 2; k = 3 would take 149
+// (one 256-thread CTA per SM, measured 1.5x slower), so it is capped at two
+// CTAs per SM. An explicit minimum of 1 CTA inflates allocation (113-136
+// registers for k <= 2, measured slower) -- hence two kernel wrappers.
+template <int K, bool ALL, bool ANG, int VEC, bool TMA>
+__global__ void __launch_bounds__(kRadialThreads + (TMA ? 32 : 0))
+radial_basis_kernel(const RadialArgs a) {
+  radial_basis_body<K, ALL, ANG, VEC, TMA>(a);
+}
+
+template <int K, bool ALL, bool ANG, int VEC, bool TMA>
+__global__ void __launch_bounds__(kRadialThreads + (TMA ? 32 : 0), 2)
+radial_basis_kernel_2cta(const RadialArgs a) {
+  radial_basis_body<K, ALL, ANG, VEC, TMA>(a);
+}
+
 // ---------------------------------------------------------------------------
 // launch
 // ---------------------------------------------------------------------------
 
 template <int K, bool ALL, bool ANG, int VEC, bool TMA>
 static cudaError_t launch_t(const RadialArgs& a, int grid, size_t smem, cudaStream_t st) {
-  auto fn = radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
+  auto fn = (K == 3 && !TMA && VEC <= 2) ? radial_basis_kernel_2cta<K, ALL, ANG, VEC, TMA>
+                                          : radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
