@@ -545,8 +545,11 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const do
     a.f = d_f;
     a.ldf = d_ldf;
     a.P = P;
+    rc = ensure_scratch(ctx, 1, zk::series_scratch_bytes(M));
+    if (rc) return rc;
     int launches = 0;
-    cudaError_t e = zk::launch_series(a, plan->order, deriv_order, st, &launches);
+    cudaError_t e = zk::launch_series(a, deriv_order, plan->host.max_jmax, M,
+                                      static_cast<double*>(ctx->scratch[1]), st, &launches);
     ctx->launches += launches;
     if (e != cudaSuccess) return cuda_fail(e, "series kernel launch");
   }
@@ -581,8 +584,23 @@ int zk_gram_accumulate(zk_ctx* ctx, const zk_plan* plan, const double* rho, cons
   int64_t Pp = budget / (Mp * 8) / 1024 * 1024;
   Pp = std::max<int64_t>(1024, std::min<int64_t>(Pp, (P + 1023) / 1024 * 1024));
   // point slices per panel: >= 2 waves of one 256-thread CTA per SM
-  int64_t ksplit = (2 * int64_t(ctx->sm_count) + ntri - 1) / ntri;
-  ksplit = std::max<int64_t>(1, std::min<int64_t>(ksplit, Pp / (16 * 32)));
+  // point slices per panel: pick the split whose CTA count (one 256-thread CTA
+  // per SM) fills the last wave best, with at least two waves
+  int64_t ksplit = 1;
+  {
+    const int64_t sms = ctx->sm_count;
+    double best = -1.0;
+    for (int64_t ks = 1; ks <= 16; ++ks) {
+      if (ks > 1 && Pp / ks < 16 * 32) break;  // keep >= 32 pipeline steps per slice
+      const int64_t n = ntri * ks;
+      const int64_t waves = (n + sms - 1) / sms;
+      const double eff = double(n) / double(waves * sms) - (waves < 2 ? 0.5 : 0.0);
+      if (eff > best + 1e-9) {
+        best = eff;
+        ksplit = ks;
+      }
+    }
+  }
   const size_t panel_b = align_up(size_t(Pp) * size_t(Mp) * 8, 256);
   const size_t part_b = align_up(size_t(ksplit) * ntri * BMg * BMg * 8, 256);
   const size_t in_b = align_up(size_t(Pp) * 8, 256);
@@ -633,7 +651,8 @@ int zk_gram_accumulate(zk_ctx* ctx, const zk_plan* plan, const double* rho, cons
       }
     }
     int launches = 0;
-    cudaError_t e = zk::launch_gram_panel(panel, Pp, Pp, M, static_cast<int>(ksplit), part, dG,
+    const int64_t kpanel = (n + 15) / 16 * 16;  // rows past n are zero; skip the rest
+    cudaError_t e = zk::launch_gram_panel(panel, Pp, kpanel, M, static_cast<int>(ksplit), part, dG,
                                           dB, st, &launches);
     ctx->launches += launches;
     if (e != cudaSuccess) return cuda_fail(e, "gram kernel launch");

@@ -82,11 +82,17 @@ struct PowSet {
   double A3, B3, C3, D3;  // (m-2)(m-1)m rho^max(m-3,0), rho^max(m-1,0), rho^(m+1), rho^(m+3)
 };
 
+// Lowest exponent the order-K assembly of mode |m| needs.
 template <int K>
-__device__ __forceinline__ PowSet<K> make_powset(double rho, int m) {
+__device__ __forceinline__ int powset_base(int m) {
+  return m - K > 0 ? m - K : 0;
+}
+
+// PowSet from acc = rho^powset_base<K>(m) in double-double.
+template <int K>
+__device__ __forceinline__ PowSet<K> make_powset_from(dd acc, double rho, int m) {
   PowSet<K> s;
-  const int e_lo = m - K > 0 ? m - K : 0;
-  dd acc = dd_pow(rho, e_lo);
+  const int e_lo = powset_base<K>(m);
   const int em1 = m - 1 > 0 ? m - 1 : 0;
   const int em2 = m - 2 > 0 ? m - 2 : 0;
   const int em3 = m - 3 > 0 ? m - 3 : 0;
@@ -116,6 +122,11 @@ __device__ __forceinline__ PowSet<K> make_powset(double rho, int m) {
   s.C3 = p_p1;
   s.D3 = p_p3;
   return s;
+}
+
+template <int K>
+__device__ __forceinline__ PowSet<K> make_powset(double rho, int m) {
+  return make_powset_from<K>(dd_pow(rho, powset_base<K>(m)), rho, m);
 }
 
 // Radial value of order O from the chain values ch[i] = P_{j-i}^{(m+i,i)}(u),

@@ -54,8 +54,9 @@ struct SeriesArgs {
   long long P;
 };
 
-cudaError_t launch_series(const SeriesArgs& a, const int32_t* order, int K, cudaStream_t st,
-                          int* launches);
+size_t series_scratch_bytes(long long ncols_total);
+cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long ncols_total,
+                          double* cs, cudaStream_t st, int* launches);
 
 size_t gram_smem_bytes();
 cudaError_t launch_gram_panel(const double* panel, long long ld, long long kpanel, long long M,

@@ -6,12 +6,18 @@
 // assembly, same angular factor), and folded into NC running sums per point
 // instead of being stored: the 15 GB basis of config 5 never exists.
 //
-// Decomposition: a CTA owns kPts points and kSlices alpha-slices. Warp w works
-// on points (w % kPtsWarps)*32.. and on the alpha groups whose launch slot is
-// congruent to its slice (heaviest-first order, so slices balance); the
-// slices' partial sums are reduced in a fixed order through shared memory, so
-// results are deterministic.
+// Decomposition: one CTA owns a tile of kThreads*VEC points and walks every
+// alpha group of the plan in ascending alpha; each thread carries VEC points.
+// Per group, the recursion coefficients / prefactors / row pointers are
+// staged into shared memory with cp.async one group ahead (double buffer, one
+// barrier per group). rho^alpha is advanced incrementally in double-double
+// (groups ascend in alpha), so the per-group power costs one DD product
+// instead of a binary exponentiation. The coefficient vectors are gathered
+// once per call into plan column order (series_gather_kernel), so each
+// group's coefficients are one contiguous, warp-uniform run.
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "zk_kernels.cuh"
 #include "zk_launch.h"
@@ -19,126 +25,261 @@
 namespace zk {
 
 namespace {
-constexpr int kPts = 64;      // points per CTA
-constexpr int kSlices = 4;    // alpha slices per CTA
-constexpr int kThreads = kPts * kSlices;
+constexpr int kThreads = 256;
+constexpr int kVec = 2;
+constexpr int kTile = kThreads * kVec;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
 }  // namespace
+
+// cs[r*NCt + v] = c[col(r) + (v0+v)*ldc] in plan column-slot order
+__global__ void series_gather_kernel(const int32_t* __restrict__ cols, long long ncols_total,
+                                     const double* __restrict__ c, long long ldc, int v0, int nc,
+                                     double* __restrict__ cs) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= ncols_total * nc) return;
+  const long long r = t / nc;
+  const int v = static_cast<int>(t - r * nc);
+  cs[t] = c[(cols[r] >> 1) + (v0 + v) * ldc];
+}
 
 template <int K, bool ANG, int NC>
 __global__ void __launch_bounds__(kThreads)
-series_kernel(const SeriesArgs a, const int32_t* __restrict__ order, int v0) {
-  __shared__ double s_acc[kSlices][NC][kPts];
+series_kernel(const SeriesArgs a, const double* __restrict__ cs, int v0, int buf_doubles) {
+  extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x;
-  const int lp = tid % kPts;
-  const int slice = tid / kPts;
-  const long long p = static_cast<long long>(blockIdx.x) * kPts + lp;
-  const bool live = p < a.P;
-  const double rho = live ? __ldg(a.rho + p) : 0.0;
-  const double theta = (ANG && live) ? __ldg(a.theta + p) : 0.0;
-  const double u = jacobi_u(rho);
+  const long long p0 = static_cast<long long>(blockIdx.x) * kTile + tid * kVec;
 
-  double acc[NC];
+  double rho[kVec], u[kVec], th[kVec];
+  dd pw_acc[kVec];
 #pragma unroll
-  for (int v = 0; v < NC; ++v) acc[v] = 0.0;
+  for (int v = 0; v < kVec; ++v) {
+    const bool live = p0 + v < a.P;
+    rho[v] = live ? __ldg(a.rho + p0 + v) : 0.0;
+    th[v] = (ANG && live) ? __ldg(a.theta + p0 + v) : 0.0;
+    u[v] = jacobi_u(rho[v]);
+    pw_acc[v] = dd{1.0, 0.0};
+  }
+  int e_cur = 0;
+  double acc[NC][kVec];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int v = 0; v < kVec; ++v) acc[c][v] = 0.0;
 
-  for (int gs = slice; gs < a.ngroups; gs += kSlices) {
-    const GroupRec g = a.groups[order[gs]];
+  // stage group gi's coefficients, prefactors and row pointers into buffer b
+  auto stage = [&](int gi, int b) {
+    const GroupRec g = a.groups[gi];
+    const int nj = g.jmax + 1;
+    double* base = smem + b * buf_doubles;
+    const double* csrc = reinterpret_cast<const double*>(a.coef + g.coef_off);
+    const int ncoef = (K + 1) * nj * 6;
+    for (int t = tid; t < ncoef; t += kThreads) cp_async8(base + t, csrc + t);
+    double* abase = base + ncoef;
+    if (K > 0) {
+      const double* asrc = reinterpret_cast<const double*>(a.asmc + g.asm_off);
+      for (int t = tid; t < nj * 8; t += kThreads) cp_async8(abase + t, asrc + t);
+    }
+    int* rbase = reinterpret_cast<int*>(abase + (K > 0 ? nj * 8 : 0));
+    for (int t = tid; t <= nj; t += kThreads) cp_async4(rbase + t, a.rowptr + g.row0 + t);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  stage(0, 0);
+  for (int gi = 0; gi < a.ngroups; ++gi) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // buffer gi&1 ready; everyone is done with buffer (gi+1)&1
+    if (gi + 1 < a.ngroups) stage(gi + 1, (gi + 1) & 1);
+
+    const GroupRec g = a.groups[gi];
     const int alpha = g.alpha;
     const int jmax = g.jmax;
     const int nj = jmax + 1;
-    const ChainCoef* coef = a.coef + g.coef_off;
-    const AsmCoef* asmc = a.asmc + g.asm_off;
-    const int32_t* rowptr = a.rowptr + g.row0;
-    const PowSet<K> pw = make_powset<K>(rho, alpha);
-    double cs = 1.0, sn = 0.0;
-    if (ANG) sincos(__dmul_rn(static_cast<double>(alpha), theta), &sn, &cs);
-    double cur[K + 1], prev[K + 1];
+    const double* base = smem + (gi & 1) * buf_doubles;
+    const ChainCoef* s_coef = reinterpret_cast<const ChainCoef*>(base);
+    const AsmCoef* s_asm = reinterpret_cast<const AsmCoef*>(base + (K + 1) * nj * 6);
+    const int* s_row = reinterpret_cast<const int*>(base + (K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0));
+    const int row_base = s_row[0];
+
+    // rho powers: advance the double-double accumulator to rho^base (alpha ascends)
+    const int e_lo = powset_base<K>(alpha);
+    PowSet<K> pw[kVec];
+    double cs_a[kVec], sn_a[kVec];
 #pragma unroll
-    for (int i = 0; i <= K; ++i) cur[i] = prev[i] = 0.0;
-    for (int j = 0; j <= jmax; ++j) {
+    for (int v = 0; v < kVec; ++v) {
+      if (e_lo > e_cur) pw_acc[v] = dd_mul(pw_acc[v], dd_pow(rho[v], e_lo - e_cur));
+      pw[v] = make_powset_from<K>(pw_acc[v], rho[v], alpha);
+      cs_a[v] = 1.0;
+      sn_a[v] = 0.0;
+      if (ANG) sincos(__dmul_rn(static_cast<double>(alpha), th[v]), &sn_a[v], &cs_a[v]);
+    }
+    e_cur = e_lo > e_cur ? e_lo : e_cur;
+
+    // fold degree j's value into the running sums; STEADY: all chains >= 2
+    auto fold = [&](int j, const double(&chs)[K + 1][kVec], auto steady) {
+      const int r_lo = s_row[j] - row_base, r_hi = s_row[j + 1] - row_base;
+      if (r_lo == r_hi) return;
+      AsmCoef ac;
+      if constexpr (K > 0) ac = s_asm[j];
+      double val[kVec];
+#pragma unroll
+      for (int v = 0; v < kVec; ++v) {
+        double ch[K + 1];
+#pragma unroll
+        for (int i = 0; i <= K; ++i)
+          ch[i] = (decltype(steady)::value || j - i >= 0) ? chs[i][v] : 0.0;
+        const double x = assemble<K, K>(pw[v], ac, ch);
+        val[v] = (j & 1) ? -x : x;
+      }
+      for (int r = r_lo; r < r_hi; ++r) {
+        const long long slot = row_base + r;
+        double w[kVec];
+        if constexpr (ANG) {
+          const bool neg_m = (__ldg(a.cols + slot) & 1) != 0;
+#pragma unroll
+          for (int v = 0; v < kVec; ++v) w[v] = __dmul_rn(val[v], neg_m ? sn_a[v] : cs_a[v]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < kVec; ++v) w[v] = val[v];
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const double cv = __ldg(cs + slot * NC + c);
+#pragma unroll
+          for (int v = 0; v < kVec; ++v) acc[c][v] = fma(w[v], cv, acc[c][v]);
+        }
+      }
+    };
+
+    double A[K + 1][kVec], B[K + 1][kVec];  // A: newest degree, B: the one before
+    const int j_pro = min(jmax, K + 1);
+    for (int j = 0; j <= j_pro; ++j) {
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
         const int d = j - i;
-        if (d >= 2) {
-          const ChainCoef c = coef[i * nj + d];
-          const double nx = jacobi_step(c, u, cur[i], prev[i]);
-          prev[i] = cur[i];
-          cur[i] = nx;
+        if (d == 0) {
+#pragma unroll
+          for (int v = 0; v < kVec; ++v) A[i][v] = 1.0;
         } else if (d == 1) {
-          prev[i] = cur[i];
-          cur[i] = jacobi_p1(static_cast<double>(alpha + i + 1),
-                             static_cast<double>(alpha + 2 * i + 2), u);
-        } else if (d == 0) {
-          cur[i] = 1.0;
+          const double a1 = static_cast<double>(alpha + i + 1);
+          const double ab2 = static_cast<double>(alpha + 2 * i + 2);
+#pragma unroll
+          for (int v = 0; v < kVec; ++v) {
+            B[i][v] = A[i][v];
+            A[i][v] = jacobi_p1(a1, ab2, u[v]);
+          }
+        } else if (d >= 2) {
+          const ChainCoef c = s_coef[i * nj + d];
+#pragma unroll
+          for (int v = 0; v < kVec; ++v) {
+            const double nx = jacobi_step(c, u[v], A[i][v], B[i][v]);
+            B[i][v] = A[i][v];
+            A[i][v] = nx;
+          }
         }
       }
-      const int r_lo = __ldg(rowptr + j), r_hi = __ldg(rowptr + j + 1);
-      if (r_lo == r_hi) continue;
-      AsmCoef ac;
-      if constexpr (K > 0) ac = asmc[j];
-      double ch[K + 1];
+      fold(j, A, std::false_type{});
+    }
+    int j = K + 2;
+    for (; j + 1 <= jmax; j += 2) {
 #pragma unroll
-      for (int i = 0; i <= K; ++i) ch[i] = (j - i >= 0) ? cur[i] : 0.0;
-      double val = assemble<K, K>(pw, ac, ch);
-      val = (j & 1) ? -val : val;
-      for (int r = r_lo; r < r_hi; ++r) {
-        const int code = __ldg(a.cols + r);
-        const long long col = code >> 1;
-        const double w = ANG ? __dmul_rn(val, (code & 1) ? sn : cs) : val;
+      for (int i = 0; i <= K; ++i) {
+        const ChainCoef c = s_coef[i * nj + (j - i)];
 #pragma unroll
-        for (int v = 0; v < NC; ++v) acc[v] = fma(w, __ldg(a.c + col + (v0 + v) * a.ldc), acc[v]);
+        for (int v = 0; v < kVec; ++v) B[i][v] = jacobi_step(c, u[v], A[i][v], B[i][v]);
       }
+      fold(j, B, std::true_type{});
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        const ChainCoef c = s_coef[i * nj + (j + 1 - i)];
+#pragma unroll
+        for (int v = 0; v < kVec; ++v) A[i][v] = jacobi_step(c, u[v], B[i][v], A[i][v]);
+      }
+      fold(j + 1, A, std::true_type{});
+    }
+    if (j <= jmax) {
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        const ChainCoef c = s_coef[i * nj + (j - i)];
+#pragma unroll
+        for (int v = 0; v < kVec; ++v) B[i][v] = jacobi_step(c, u[v], A[i][v], B[i][v]);
+      }
+      fold(j, B, std::true_type{});
     }
   }
 #pragma unroll
-  for (int v = 0; v < NC; ++v) s_acc[slice][v][lp] = acc[v];
-  __syncthreads();
-  if (slice == 0 && live) {
+  for (int c = 0; c < NC; ++c)
 #pragma unroll
-    for (int v = 0; v < NC; ++v) {
-      double s = s_acc[0][v][lp];
-#pragma unroll
-      for (int t = 1; t < kSlices; ++t) s += s_acc[t][v][lp];
-      a.f[p + (v0 + v) * a.ldf] = s;
-    }
-  }
+    for (int v = 0; v < kVec; ++v)
+      if (p0 + v < a.P) a.f[p0 + v + (v0 + c) * a.ldf] = acc[c][v];
 }
 
-template <int K, bool ANG>
-static cudaError_t launch_nc(const SeriesArgs& a, const int32_t* order, int v0, int nc,
-                             cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>((a.P + kPts - 1) / kPts);
-  switch (nc) {
-    case 8: series_kernel<K, ANG, 8><<<grid, kThreads, 0, st>>>(a, order, v0); break;
-    case 4: series_kernel<K, ANG, 4><<<grid, kThreads, 0, st>>>(a, order, v0); break;
-    case 2: series_kernel<K, ANG, 2><<<grid, kThreads, 0, st>>>(a, order, v0); break;
-    default: series_kernel<K, ANG, 1><<<grid, kThreads, 0, st>>>(a, order, v0); break;
+template <int K, bool ANG, int NC>
+static cudaError_t launch_one(const SeriesArgs& a, const double* cs, int v0, int buf_doubles,
+                              cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>((a.P + kTile - 1) / kTile);
+  const size_t smem = size_t(2) * buf_doubles * sizeof(double);
+  auto fn = series_kernel<K, ANG, NC>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
   }
+  fn<<<grid, kThreads, smem, st>>>(a, cs, v0, buf_doubles);
   return cudaGetLastError();
 }
 
-template <int K>
-static cudaError_t launch_ang(const SeriesArgs& a, const int32_t* order, int v0, int nc,
-                              cudaStream_t st) {
-  return a.theta ? launch_nc<K, true>(a, order, v0, nc, st)
-                 : launch_nc<K, false>(a, order, v0, nc, st);
+template <int K, bool ANG>
+static cudaError_t launch_nc(const SeriesArgs& a, const double* cs, int v0, int nc,
+                             int buf_doubles, cudaStream_t st) {
+  switch (nc) {
+    case 8: return launch_one<K, ANG, 8>(a, cs, v0, buf_doubles, st);
+    case 4: return launch_one<K, ANG, 4>(a, cs, v0, buf_doubles, st);
+    case 2: return launch_one<K, ANG, 2>(a, cs, v0, buf_doubles, st);
+    default: return launch_one<K, ANG, 1>(a, cs, v0, buf_doubles, st);
+  }
 }
 
-cudaError_t launch_series(const SeriesArgs& a, const int32_t* order, int K, cudaStream_t st,
-                          int* launches) {
+template <int K>
+static cudaError_t launch_ang(const SeriesArgs& a, const double* cs, int v0, int nc,
+                              int buf_doubles, cudaStream_t st) {
+  return a.theta ? launch_nc<K, true>(a, cs, v0, nc, buf_doubles, st)
+                 : launch_nc<K, false>(a, cs, v0, nc, buf_doubles, st);
+}
+
+size_t series_scratch_bytes(long long ncols_total) {
+  return static_cast<size_t>(ncols_total) * 8 * sizeof(double) + 256;
+}
+
+cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long ncols_total,
+                          double* cs, cudaStream_t st, int* launches) {
   if (a.P <= 0) return cudaSuccess;
+  const int nj = max_jmax + 1;
+  // per-group stage: (K+1) chains x nj ChainCoef, nj AsmCoef, nj+1 row pointers
+  const int buf_doubles = ((K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0) + (nj + 2) / 2 + 1 + 1) & ~1;
   for (int v0 = 0; v0 < a.ncoef;) {
     const int left = a.ncoef - v0;
     const int nc = left >= 8 ? 8 : left >= 4 ? 4 : left >= 2 ? 2 : 1;
-    cudaError_t e;
+    const long long n = ncols_total * nc;
+    series_gather_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+        a.cols, ncols_total, a.c, a.ldc, v0, nc, cs);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     switch (K) {
-      case 0: e = launch_ang<0>(a, order, v0, nc, st); break;
-      case 1: e = launch_ang<1>(a, order, v0, nc, st); break;
-      case 2: e = launch_ang<2>(a, order, v0, nc, st); break;
-      default: e = launch_ang<3>(a, order, v0, nc, st); break;
+      case 0: e = launch_ang<0>(a, cs, v0, nc, buf_doubles, st); break;
+      case 1: e = launch_ang<1>(a, cs, v0, nc, buf_doubles, st); break;
+      case 2: e = launch_ang<2>(a, cs, v0, nc, buf_doubles, st); break;
+      default: e = launch_ang<3>(a, cs, v0, nc, buf_doubles, st); break;
     }
     if (e != cudaSuccess) return e;
-    ++*launches;
+    *launches += 2;
     v0 += nc;
   }
   return cudaSuccess;
