@@ -15,7 +15,8 @@ from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_uint32, c_void_
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libzk_b200.so")
+LIB_PATH = os.environ.get("ZK_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "libzk_b200.so")
 
 ZK_OK = 0
 ZK_EINVAL = -1

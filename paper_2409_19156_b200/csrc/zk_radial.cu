@@ -39,16 +39,30 @@ constexpr int kComputeWarps = kRadialThreads / 32;
 constexpr int kRingStages = 4;  // TMA staging ring depth
 constexpr int kRingLag = 1;     // bulk groups the producer keeps in flight before releasing
 
+// L2 policy for the basis stream: evict-first. The output is written once and
+// never re-read by this kernel; marking it evict-first lets L2 drain it to HBM
+// ahead of anything else. Measured at config 2: 0.598 ms vs 0.615 ms plain
+// (6.9 vs 6.7 TB/s); .cs / L1::no_allocate hints made no difference.
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 template <int VEC>
-__device__ __forceinline__ void store_vec(double* dst, const double (&w)[VEC]) {
+__device__ __forceinline__ void store_vec(double* dst, const double (&w)[VEC],
+                                          unsigned long long pol) {
   if constexpr (VEC == 4) {
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(dst), "d"(w[0]), "d"(w[1]),
-                 "d"(w[2]), "d"(w[3])
+    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst),
+                 "d"(w[0]), "d"(w[1]), "d"(w[2]), "d"(w[3]), "l"(pol)
                  : "memory");
   } else if constexpr (VEC == 2) {
-    *reinterpret_cast<double2*>(dst) = make_double2(w[0], w[1]);
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(dst), "d"(w[0]),
+                 "d"(w[1]), "l"(pol)
+                 : "memory");
   } else {
-    *dst = w[0];
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(dst), "d"(w[0]), "l"(pol)
+                 : "memory");
   }
 }
 
@@ -263,6 +277,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
       }
     }
     char* obase = reinterpret_cast<char*>(a.out + p0);
+    const unsigned long long pol = evict_first_policy();
     const long long ostride_b = a.ostride * 8;
 
     auto emit = [&](int j, const double(&chs)[K + 1][VEC], auto steady) {
@@ -282,7 +297,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
             for (int o = 0; o < NO; ++o) {
               double w[VEC];
               th.column(ANG && (off & 1) != 0, o, val, w);
-              store_vec<VEC>(reinterpret_cast<double*>(dst + o * ostride_b), w);
+              store_vec<VEC>(reinterpret_cast<double*>(dst + o * ostride_b), w, pol);
             }
           }
         } else {
