@@ -286,3 +286,46 @@ class Workload:
 
     def modes(self) -> list[tuple[int, int]]:
         return full_modes(self.resolution)
+
+
+# --------------------------------------------------------------------------
+# binary128 oracle (oracle/zk_quad.c) -- fast high-precision check for big sweeps
+# --------------------------------------------------------------------------
+
+_QUAD = None
+
+
+def _quad_lib():
+    """Load (building on first use if needed) oracle/build/libzk_quad.so."""
+    global _QUAD
+    if _QUAD is None:
+        import ctypes
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        so = os.path.join(here, "build", "libzk_quad.so")
+        src = os.path.join(here, "zk_quad.c")
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+            os.makedirs(os.path.dirname(so), exist_ok=True)
+            subprocess.run(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", src, "-o", so,
+                            "-lquadmath"], check=True)
+        lib = ctypes.CDLL(so)
+        p = ctypes.c_void_p
+        lib.zkq_radial_table.argtypes = [p, p, ctypes.c_int64, p, ctypes.c_int64, ctypes.c_int, p]
+        lib.zkq_radial_table.restype = ctypes.c_int
+        _QUAD = lib
+    return _QUAD
+
+
+def quad_table(modes, rho, k: int = 0) -> np.ndarray:
+    """(P, M) values computed in binary128 and rounded once (see zk_quad.c)."""
+    n = np.ascontiguousarray([int(a) for a, _ in modes], dtype=np.int32)
+    m = np.ascontiguousarray([int(b) for _, b in modes], dtype=np.int32)
+    r = np.ascontiguousarray(rho, dtype=np.float64)
+    out = np.empty((n.size, r.size), dtype=np.float64)
+    if n.size and r.size:
+        rc = _quad_lib().zkq_radial_table(n.ctypes.data, m.ctypes.data, n.size, r.ctypes.data,
+                                          r.size, int(k), out.ctypes.data)
+        if rc:
+            raise ValueError("bad derivative order")
+    return out.T

@@ -82,9 +82,10 @@ __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
-               "r"(smem_addr(ssrc)), "r"(bytes)
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes,
+                                           unsigned long long pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_addr(ssrc)), "r"(bytes), "l"(pol)
                : "memory");
 }
 
@@ -219,6 +220,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
   // ---- producer warp (TMA only): replays the compute warps' stage sequence
   if (TMA && warp == kComputeWarps) {
     if (lane == 0) {
+      const unsigned long long pol = evict_first_policy();
       unsigned use = 0;
       for (int tile = t_begin; tile < t_end; ++tile) {
         const long long tile0 = static_cast<long long>(tile) * TP;
@@ -236,7 +238,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
               const int r = r_lo + q / NO;
               const int o = q - (q / NO) * NO;
               const long long off = col_offset(r) & ~1LL;
-              bulk_store(tbase + off + o * a.ostride * 8, sb + (q - q0) * TP, TP * 8);
+              bulk_store(tbase + off + o * a.ostride * 8, sb + (q - q0) * TP, TP * 8, pol);
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             if (use >= kRingLag) {

@@ -113,6 +113,43 @@ def test_config4_high_order_error_no_worse_than_reference(golden):
     assert err_gpu_g <= err_ref_g, (err_gpu_g, err_ref_g)
 
 
+def test_config4_full_grid_error_vs_binary128_oracle():
+    """The n=200 clause at scale: every mode on every 5th point of the 1e4-point
+    grid (2,000 points x 20,301 columns), max-abs error against the binary128
+    oracle (bitwise equal to the exact oracle, tests/test_oracle.py) is no worse
+    than the reference algorithm's own error on the same entries."""
+    modes = zb.full_mode_set(200)
+    grid = zb.linear_radial_grid(10_000)
+    got = radial(modes, grid, 0)[::5]
+    pts = grid[::5]
+    umodes = [(n, a) for n in range(201) for a in range(n % 2, n + 1, 2)]
+    ucols = [c for c, md in enumerate(modes) if md.m >= 0]
+    exact = orc.quad_table(umodes, pts, 0)
+    ref = orc.radial_batch(umodes, pts, 0)
+    err_gpu = float(np.abs(got[:, ucols] - exact).max())
+    err_ref = float(np.abs(ref - exact).max())
+    print(f"n<=200, 2000 pts: max-abs error gpu {err_gpu:.3e}, reference {err_ref:.3e}")
+    assert err_gpu <= err_ref, (err_gpu, err_ref)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_config2_3_error_vs_binary128_oracle(k):
+    """n<=100 on 500 points of the config-2 grid, every order: GPU error vs the
+    exact value within the north_star tolerance, and on par with the
+    reference algorithm's own error."""
+    modes = [(n, a) for n in range(101) for a in range(n % 2, n + 1, 2)]
+    grid = zb.linear_radial_grid(100_000)[::200]
+    got = radial(zb.as_mode_set(modes), grid, k)
+    exact = orc.quad_table(modes, grid, k)
+    ref = orc.radial_batch(modes, grid, k)
+    scale = np.maximum(1.0, np.abs(exact).max(axis=0))
+    e_gpu = float((np.abs(got - exact).max(axis=0) / scale).max())
+    e_ref = float((np.abs(ref - exact).max(axis=0) / scale).max())
+    print(f"k={k}: relative error gpu {e_gpu:.3e}, reference {e_ref:.3e}")
+    assert e_gpu <= 1e-12
+    assert e_gpu <= 2 * e_ref + 1e-15
+
+
 def test_config5_2d_basis_matches_golden(golden):
     modes = zb.full_mode_set(60)
     n = np.array([md.n for md in modes])

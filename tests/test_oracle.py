@@ -99,3 +99,16 @@ def test_batch_equals_single_mode():
     table = orc.radial_batch(modes, g, 2)
     for col, (n, m) in enumerate(modes):
         assert np.array_equal(table[:, col], orc.radial_single(n, abs(m), g, 2))
+
+
+def test_binary128_oracle_equals_exact_oracle(golden):
+    # the fast binary128 oracle (oracle/zk_quad.c) reproduces the reference's
+    # exact big-integer oracle bit for bit: all 16 x 10,201 golden n=200 values...
+    modes = orc.full_modes(200)
+    umodes = [modes[c] for c in golden["c4_ucols"]]
+    assert np.array_equal(orc.quad_table(umodes, golden["c4_grid"], 0), golden["c4_exact"])
+    # ...and every derivative order against the restated exact oracle
+    pts = np.array([0.0, 1e-3, 0.1, 0.37, 0.5, 0.77, 0.93, 1.0])
+    small = [(n, m) for n in range(0, 41) for m in range(-n, n + 1, 2)]
+    for k in range(4):
+        assert np.array_equal(orc.quad_table(small, pts, k), orc.exact_table(small, pts, k)), k
