@@ -591,7 +591,7 @@ int zk_gram_accumulate(zk_ctx* ctx, const zk_plan* plan, const double* rho, cons
     const int64_t sms = ctx->sm_count;
     double best = -1.0;
     for (int64_t ks = 1; ks <= 16; ++ks) {
-      if (ks > 1 && Pp / ks < 16 * 32) break;  // keep >= 32 pipeline steps per slice
+      if (ks > 1 && Pp / ks < int64_t(zk::gram_k_granule()) * 32) break;  // >= 32 steps per slice
       const int64_t n = ntri * ks;
       const int64_t waves = (n + sms - 1) / sms;
       const double eff = double(n) / double(waves * sms) - (waves < 2 ? 0.5 : 0.0);
@@ -651,7 +651,8 @@ int zk_gram_accumulate(zk_ctx* ctx, const zk_plan* plan, const double* rho, cons
       }
     }
     int launches = 0;
-    const int64_t kpanel = (n + 15) / 16 * 16;  // rows past n are zero; skip the rest
+    const int64_t gk = zk::gram_k_granule();
+    const int64_t kpanel = (n + gk - 1) / gk * gk;  // rows past n are zero; skip the rest
     cudaError_t e = zk::launch_gram_panel(panel, Pp, kpanel, M, static_cast<int>(ksplit), part, dG,
                                           dB, st, &launches);
     ctx->launches += launches;

@@ -59,6 +59,7 @@ cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nc
                           double* cs, cudaStream_t st, int* launches);
 
 size_t gram_smem_bytes();
+int gram_k_granule();  // points per SYRK pipeline step (panel rows are padded to it)
 cudaError_t launch_gram_panel(const double* panel, long long ld, long long kpanel, long long M,
                               int ksplit, double* part, double* G, double* Bty, cudaStream_t st,
                               int* launches);
