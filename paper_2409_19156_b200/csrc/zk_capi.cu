@@ -3,12 +3,16 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/zk_b200.h"
@@ -38,6 +42,76 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
 
+namespace {
+
+// Persistent host worker pool for the pageable-output scatter (a fresh numpy
+// array is pageable: the D2H lands in pinned bounce buffers and these threads
+// spread it into place, first-touching the pages in parallel).
+class HostPool {
+ public:
+  explicit HostPool(unsigned n) {
+    for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  unsigned size() const { return static_cast<unsigned>(workers_.size()) + 1; }
+  // run fn(i) for i in [0, n) on the pool and the calling thread
+  void parallel_for(int64_t n, const std::function<void(int64_t)>& fn) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      fn_ = &fn;
+      n_ = n;
+      next_.store(0);
+      active_ = static_cast<int>(workers_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> l(m_);
+    done_cv_.wait(l, [this] { return active_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void work() {
+    for (int64_t i = next_.fetch_add(1); i < n_; i = next_.fetch_add(1)) (*fn_)(i);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> l(m_);
+        cv_.wait(l, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+      }
+      work();
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (--active_ == 0) done_cv_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int64_t)>* fn_ = nullptr;
+  int64_t n_ = 0;
+  std::atomic<int64_t> next_{0};
+  int active_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+}  // namespace
+
 struct zk_ctx {
   int device = 0;
   int sm_count = 148;
@@ -49,6 +123,11 @@ struct zk_ctx {
   // device scratch for host-pointer calls: per pipeline slot
   void* scratch[2] = {nullptr, nullptr};
   size_t scratch_bytes[2] = {0, 0};
+  // pinned bounce buffers + events for pageable host outputs, per slot
+  void* hbounce[2] = {nullptr, nullptr};
+  size_t hbounce_bytes[2] = {0, 0};
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  HostPool* pool = nullptr;
   int64_t launches = 0;
   std::mutex mu;  // one call at a time per ctx
 };
@@ -238,10 +317,39 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
   // the pipeline must start after work already queued on the launch stream
   ZK_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
   for (int s = 0; s < 2; ++s) ZK_CUDA(cudaStreamWaitEvent(ctx->pipe[s], ctx->ev_start, 0));
-  int64_t chunk = 0;
-  for (int64_t p0 = 0; p0 < P; p0 += pc, ++chunk) {
+  // pageable destination (e.g. a fresh numpy array): D2H into pinned bounce
+  // buffers, then the host pool scatters each chunk into place in parallel
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  const bool bounce = !pinned && env_int("ZK_BOUNCE", 1) != 0;
+  if (bounce) {
+    for (int s = 0; s < 2; ++s) {
+      if (ctx->hbounce_bytes[s] < basis_bytes) {
+        if (ctx->hbounce[s]) {
+          cudaFreeHost(ctx->hbounce[s]);
+          ctx->hbounce[s] = nullptr;
+          ctx->hbounce_bytes[s] = 0;
+        }
+        cudaError_t e = cudaHostAlloc(&ctx->hbounce[s], basis_bytes, cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          return fail(ZK_ENOMEM, std::string("pinned bounce buffer: ") + cudaGetErrorString(e));
+        }
+        ctx->hbounce_bytes[s] = basis_bytes;
+      }
+    }
+    if (!ctx->pool) {
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+      ctx->pool = new HostPool(std::min(15u, hw - 1));
+    }
+  }
+  const int64_t nchunks = (P + pc - 1) / pc;
+  auto enqueue = [&](int64_t chunk) -> int {
     const int s = static_cast<int>(chunk & 1);
     cudaStream_t st = ctx->pipe[s];
+    const int64_t p0 = chunk * pc;
     const int64_t n = std::min<int64_t>(pc, P - p0);
     double* dbasis = static_cast<double*>(ctx->scratch[s]);
     double* din = reinterpret_cast<double*>(static_cast<char*>(ctx->scratch[s]) + basis_bytes);
@@ -259,10 +367,43 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
     const int64_t dld = pc;
     int rc = launch_device(ctx, plan, r_in, t_in, n, k, all, dbasis, dld, dld * M, scalar, st);
     if (rc) return rc;
-    for (int o = 0; o < NO; ++o) {
-      ZK_CUDA(cudaMemcpy2DAsync(out + o * ostride + p0, size_t(ld) * 8, dbasis + o * dld * M,
-                                size_t(dld) * 8, size_t(n) * 8, size_t(M),
-                                cudaMemcpyDeviceToHost, st));
+    if (bounce) {
+      ZK_CUDA(cudaMemcpyAsync(ctx->hbounce[s], dbasis, size_t(dld) * M * NO * 8,
+                              cudaMemcpyDeviceToHost, st));
+      ZK_CUDA(cudaEventRecord(ctx->ev_done[s], st));
+    } else {
+      for (int o = 0; o < NO; ++o) {
+        ZK_CUDA(cudaMemcpy2DAsync(out + o * ostride + p0, size_t(ld) * 8, dbasis + o * dld * M,
+                                  size_t(dld) * 8, size_t(n) * 8, size_t(M),
+                                  cudaMemcpyDeviceToHost, st));
+      }
+    }
+    return ZK_OK;
+  };
+  if (!bounce) {
+    for (int64_t c = 0; c < nchunks; ++c) {
+      int rc = enqueue(c);
+      if (rc) return rc;
+    }
+  } else {
+    for (int64_t c = 0; c < std::min<int64_t>(2, nchunks); ++c) {
+      int rc = enqueue(c);
+      if (rc) return rc;
+    }
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int s = static_cast<int>(c & 1);
+      ZK_CUDA(cudaEventSynchronize(ctx->ev_done[s]));
+      const int64_t p0 = c * pc;
+      const int64_t n = std::min<int64_t>(pc, P - p0);
+      const double* hb = static_cast<const double*>(ctx->hbounce[s]);
+      ctx->pool->parallel_for(int64_t(NO) * M, [&](int64_t oc) {
+        const int64_t o = oc / M, col = oc - o * M;
+        std::memcpy(out + o * ostride + col * ld + p0, hb + (o * M + col) * pc, size_t(n) * 8);
+      });
+      if (c + 2 < nchunks) {
+        int rc = enqueue(c + 2);
+        if (rc) return rc;
+      }
     }
   }
   ZK_CUDA(cudaStreamSynchronize(ctx->pipe[0]));
@@ -318,6 +459,8 @@ int zk_ctx_create(int device, zk_ctx** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pipe[0], cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pipe[1], cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming);
+  for (int s = 0; s < 2 && e == cudaSuccess; ++s)
+    e = cudaEventCreateWithFlags(&ctx->ev_done[s], cudaEventDisableTiming | cudaEventBlockingSync);
   if (e != cudaSuccess) {
     zk_ctx_destroy(ctx);
     return cuda_fail(e, "context creation");
@@ -340,6 +483,11 @@ int zk_ctx_destroy(zk_ctx* ctx) {
     cudaStreamDestroy(ctx->own);
   }
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+  for (int s = 0; s < 2; ++s) {
+    if (ctx->ev_done[s]) cudaEventDestroy(ctx->ev_done[s]);
+    if (ctx->hbounce[s]) cudaFreeHost(ctx->hbounce[s]);
+  }
+  delete ctx->pool;
   delete ctx;
   return ZK_OK;
 }
