@@ -216,7 +216,9 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
   };
   int vec = 1;
   if (!force_scalar) {
-    const int want = env_int("ZK_VEC", K == 0 ? 4 : 2);
+    // 4 points per thread for the plain radial k=0 basis, 2 when the thread also
+    // carries the angular factors or derivative chains (register budget)
+    const int want = env_int("ZK_VEC", (K == 0 && theta == nullptr) ? 4 : 2);
     for (int v : {4, 2}) {
       if (v <= want && fits(v)) {
         vec = v;
