@@ -381,3 +381,39 @@ def test_heavily_duplicated_group_is_split():
     ref = orc.radial_batch(pairs, grid, 1)
     assert within_tolerance(got, ref)
     assert np.array_equal(got[:, 0], got[:, 4999])
+
+
+def test_high_degree_sparse_request():
+    """Degrees far beyond the configs (n up to 1000, jacobi degree 500): the
+    shared-memory coefficient stage scales with jmax; values follow the
+    reference algorithm (bitwise recursion) and the binary128 oracle."""
+    pairs = [(1000, 0), (1000, 2), (999, 999), (998, -4), (601, 11), (500, 500), (2, 2)]
+    modes = zb.as_mode_set(pairs)
+    grid = np.concatenate([[0.0, 1.0], np.random.default_rng(12).uniform(size=50)])
+    for k in (0, 2):
+        got = radial(modes, grid, k)
+        ref = orc.radial_batch(pairs, grid, k)
+        exact = orc.quad_table(pairs, grid, k)
+        err_gpu = np.abs(got - exact).max(axis=0)
+        err_ref = np.abs(ref - exact).max(axis=0)
+        assert (err_gpu <= 2 * err_ref + 1e-12 * np.maximum(1, np.abs(exact).max(axis=0))).all(), k
+
+
+def test_concurrent_callers_share_a_context():
+    """The reference drives this path from thread pools (zk/batch.py:136-138):
+    concurrent calls on one context serialise safely and agree bitwise."""
+    from concurrent.futures import ThreadPoolExecutor
+    modes = zb.full_mode_set(30)
+    grid = zb.linear_radial_grid(777)
+    want = radial(modes, grid, 1)
+    with ThreadPoolExecutor(8) as pool:
+        outs = list(pool.map(lambda _: radial(modes, grid, 1), range(16)))
+    for o in outs:
+        assert np.array_equal(o, want)
+
+
+def test_mode_set_too_large_fails_loudly():
+    # jacobi degree 3000 with k=3 cannot stage its coefficients in shared memory
+    modes = zb.as_mode_set([(6000, 0)])
+    with pytest.raises(ValueError):
+        radial(modes, [0.5], 3)
