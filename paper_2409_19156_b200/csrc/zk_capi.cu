@@ -695,10 +695,11 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const do
     a.f = d_f;
     a.ldf = d_ldf;
     a.P = P;
-    rc = ensure_scratch(ctx, 1, zk::series_scratch_bytes(M));
+    const int64_t nrowslots = static_cast<int64_t>(plan->host.rowptr.size());
+    rc = ensure_scratch(ctx, 1, zk::series_scratch_bytes(nrowslots));
     if (rc) return rc;
     int launches = 0;
-    cudaError_t e = zk::launch_series(a, deriv_order, plan->host.max_jmax, M,
+    cudaError_t e = zk::launch_series(a, deriv_order, plan->host.max_jmax, nrowslots,
                                       static_cast<double*>(ctx->scratch[1]), st, &launches);
     ctx->launches += launches;
     if (e != cudaSuccess) return cuda_fail(e, "series kernel launch");

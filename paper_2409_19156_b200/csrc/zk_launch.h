@@ -54,9 +54,9 @@ struct SeriesArgs {
   long long P;
 };
 
-size_t series_scratch_bytes(long long ncols_total);
-cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long ncols_total,
-                          double* cs, cudaStream_t st, int* launches);
+size_t series_scratch_bytes(long long nrowslots);
+cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nrowslots,
+                          double* rowc, cudaStream_t st, int* launches);
 
 size_t gram_smem_bytes();
 int gram_k_granule();  // points per SYRK pipeline step (panel rows are padded to it)

@@ -12,9 +12,14 @@
 // staged into shared memory with cp.async one group ahead (double buffer, one
 // barrier per group). rho^alpha is advanced incrementally in double-double
 // (groups ascend in alpha), so the per-group power costs one DD product
-// instead of a binary exponentiation. The coefficient vectors are gathered
-// once per call into plan column order (series_gather_kernel), so each
-// group's coefficients are one contiguous, warp-uniform run.
+// instead of a binary exponentiation.
+//
+// All columns of one (alpha, j) key share the radial value, so the
+// coefficients are folded per key once per call (series_rowsum_kernel):
+// C+ = (-1)^j sum c over m >= 0 columns, C- = (-1)^j sum c over m < 0 columns
+// (radial series: C+ over all columns). Per key and point the kernel then
+// does acc += R * (C+ cos(|m| theta) + C- sin(|m| theta)) -- no per-column
+// work at all. Only the summation order differs from B @ c (tolerance-equal).
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -39,20 +44,33 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }
 }  // namespace
 
-// cs[r*NCt + v] = c[col(r) + (v0+v)*ldc] in plan column-slot order
-__global__ void series_gather_kernel(const int32_t* __restrict__ cols, long long ncols_total,
+// rowc[(row0 + j) * 2NC + 2v + {0,1}] = (-1)^j * (C+, C-) of key (alpha, j)
+template <bool ANG>
+__global__ void series_rowsum_kernel(const GroupRec* __restrict__ groups,
+                                     const int32_t* __restrict__ rowptr,
+                                     const int32_t* __restrict__ cols,
                                      const double* __restrict__ c, long long ldc, int v0, int nc,
-                                     double* __restrict__ cs) {
-  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= ncols_total * nc) return;
-  const long long r = t / nc;
-  const int v = static_cast<int>(t - r * nc);
-  cs[t] = c[(cols[r] >> 1) + (v0 + v) * ldc];
+                                     double* __restrict__ rowc) {
+  const GroupRec g = groups[blockIdx.x];
+  for (int j = threadIdx.x; j <= g.jmax; j += blockDim.x) {
+    const int r_lo = rowptr[g.row0 + j], r_hi = rowptr[g.row0 + j + 1];
+    const double sgn = (j & 1) ? -1.0 : 1.0;
+    for (int v = 0; v < nc; ++v) {
+      double cp = 0.0, cn = 0.0;
+      for (int r = r_lo; r < r_hi; ++r) {
+        const int code = cols[r];
+        const double x = c[(code >> 1) + static_cast<long long>(v0 + v) * ldc];
+        if (ANG && (code & 1)) cn += x; else cp += x;
+      }
+      rowc[(static_cast<long long>(g.row0) + j) * 2 * nc + 2 * v] = sgn * cp;
+      rowc[(static_cast<long long>(g.row0) + j) * 2 * nc + 2 * v + 1] = sgn * cn;
+    }
+  }
 }
 
 template <int K, bool ANG, int NC>
 __global__ void __launch_bounds__(kThreads)
-series_kernel(const SeriesArgs a, const double* __restrict__ cs, int v0, int buf_doubles) {
+series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int buf_doubles) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x;
   const long long p0 = static_cast<long long>(blockIdx.x) * kTile + tid * kVec;
@@ -87,8 +105,9 @@ series_kernel(const SeriesArgs a, const double* __restrict__ cs, int v0, int buf
       const double* asrc = reinterpret_cast<const double*>(a.asmc + g.asm_off);
       for (int t = tid; t < nj * 8; t += kThreads) cp_async8(abase + t, asrc + t);
     }
-    int* rbase = reinterpret_cast<int*>(abase + (K > 0 ? nj * 8 : 0));
-    for (int t = tid; t <= nj; t += kThreads) cp_async4(rbase + t, a.rowptr + g.row0 + t);
+    double* rbase = abase + (K > 0 ? nj * 8 : 0);
+    const double* rsrc = rowc + static_cast<long long>(g.row0) * 2 * NC;
+    for (int t = tid; t < nj * 2 * NC; t += kThreads) cp_async8(rbase + t, rsrc + t);
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
@@ -105,8 +124,7 @@ series_kernel(const SeriesArgs a, const double* __restrict__ cs, int v0, int buf
     const double* base = smem + (gi & 1) * buf_doubles;
     const ChainCoef* s_coef = reinterpret_cast<const ChainCoef*>(base);
     const AsmCoef* s_asm = reinterpret_cast<const AsmCoef*>(base + (K + 1) * nj * 6);
-    const int* s_row = reinterpret_cast<const int*>(base + (K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0));
-    const int row_base = s_row[0];
+    const double* s_rc = base + (K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0);
 
     // rho powers: advance the double-double accumulator to rho^base (alpha ascends)
     const int e_lo = powset_base<K>(alpha);
@@ -124,8 +142,6 @@ series_kernel(const SeriesArgs a, const double* __restrict__ cs, int v0, int buf
 
     // fold degree j's value into the running sums; STEADY: all chains >= 2
     auto fold = [&](int j, const double(&chs)[K + 1][kVec], auto steady) {
-      const int r_lo = s_row[j] - row_base, r_hi = s_row[j + 1] - row_base;
-      if (r_lo == r_hi) return;
       AsmCoef ac;
       if constexpr (K > 0) ac = s_asm[j];
       double val[kVec];
@@ -135,25 +151,15 @@ series_kernel(const SeriesArgs a, const double* __restrict__ cs, int v0, int buf
 #pragma unroll
         for (int i = 0; i <= K; ++i)
           ch[i] = (decltype(steady)::value || j - i >= 0) ? chs[i][v] : 0.0;
-        const double x = assemble<K, K>(pw[v], ac, ch);
-        val[v] = (j & 1) ? -x : x;
+        val[v] = assemble<K, K>(pw[v], ac, ch);
       }
-      for (int r = r_lo; r < r_hi; ++r) {
-        const long long slot = row_base + r;
-        double w[kVec];
-        if constexpr (ANG) {
-          const bool neg_m = (__ldg(a.cols + slot) & 1) != 0;
 #pragma unroll
-          for (int v = 0; v < kVec; ++v) w[v] = __dmul_rn(val[v], neg_m ? sn_a[v] : cs_a[v]);
-        } else {
+      for (int c = 0; c < NC; ++c) {
+        const double2 cpn = *reinterpret_cast<const double2*>(s_rc + (j * NC + c) * 2);
 #pragma unroll
-          for (int v = 0; v < kVec; ++v) w[v] = val[v];
-        }
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const double cv = __ldg(cs + slot * NC + c);
-#pragma unroll
-          for (int v = 0; v < kVec; ++v) acc[c][v] = fma(w[v], cv, acc[c][v]);
+        for (int v = 0; v < kVec; ++v) {
+          const double w = ANG ? fma(cpn.x, cs_a[v], cpn.y * sn_a[v]) : cpn.x;
+          acc[c][v] = fma(val[v], w, acc[c][v]);
         }
       }
     };
@@ -222,7 +228,7 @@ series_kernel(const SeriesArgs a, const double* __restrict__ cs, int v0, int buf
 }
 
 template <int K, bool ANG, int NC>
-static cudaError_t launch_one(const SeriesArgs& a, const double* cs, int v0, int buf_doubles,
+static cudaError_t launch_one(const SeriesArgs& a, const double* rowc, int v0, int buf_doubles,
                               cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>((a.P + kTile - 1) / kTile);
   const size_t smem = size_t(2) * buf_doubles * sizeof(double);
@@ -232,51 +238,55 @@ static cudaError_t launch_one(const SeriesArgs& a, const double* cs, int v0, int
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  fn<<<grid, kThreads, smem, st>>>(a, cs, v0, buf_doubles);
+  fn<<<grid, kThreads, smem, st>>>(a, rowc, v0, buf_doubles);
   return cudaGetLastError();
 }
 
 template <int K, bool ANG>
-static cudaError_t launch_nc(const SeriesArgs& a, const double* cs, int v0, int nc,
+static cudaError_t launch_nc(const SeriesArgs& a, const double* rowc, int v0, int nc,
                              int buf_doubles, cudaStream_t st) {
   switch (nc) {
-    case 8: return launch_one<K, ANG, 8>(a, cs, v0, buf_doubles, st);
-    case 4: return launch_one<K, ANG, 4>(a, cs, v0, buf_doubles, st);
-    case 2: return launch_one<K, ANG, 2>(a, cs, v0, buf_doubles, st);
-    default: return launch_one<K, ANG, 1>(a, cs, v0, buf_doubles, st);
+    case 8: return launch_one<K, ANG, 8>(a, rowc, v0, buf_doubles, st);
+    case 4: return launch_one<K, ANG, 4>(a, rowc, v0, buf_doubles, st);
+    case 2: return launch_one<K, ANG, 2>(a, rowc, v0, buf_doubles, st);
+    default: return launch_one<K, ANG, 1>(a, rowc, v0, buf_doubles, st);
   }
 }
 
 template <int K>
-static cudaError_t launch_ang(const SeriesArgs& a, const double* cs, int v0, int nc,
+static cudaError_t launch_ang(const SeriesArgs& a, const double* rowc, int v0, int nc,
                               int buf_doubles, cudaStream_t st) {
-  return a.theta ? launch_nc<K, true>(a, cs, v0, nc, buf_doubles, st)
-                 : launch_nc<K, false>(a, cs, v0, nc, buf_doubles, st);
+  return a.theta ? launch_nc<K, true>(a, rowc, v0, nc, buf_doubles, st)
+                 : launch_nc<K, false>(a, rowc, v0, nc, buf_doubles, st);
 }
 
-size_t series_scratch_bytes(long long ncols_total) {
-  return static_cast<size_t>(ncols_total) * 8 * sizeof(double) + 256;
+size_t series_scratch_bytes(long long nrowslots) {
+  return static_cast<size_t>(nrowslots) * 2 * 8 * sizeof(double) + 256;
 }
 
-cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long ncols_total,
-                          double* cs, cudaStream_t st, int* launches) {
+cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nrowslots,
+                          double* rowc, cudaStream_t st, int* launches) {
+  (void)nrowslots;
   if (a.P <= 0) return cudaSuccess;
   const int nj = max_jmax + 1;
-  // per-group stage: (K+1) chains x nj ChainCoef, nj AsmCoef, nj+1 row pointers
-  const int buf_doubles = ((K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0) + (nj + 2) / 2 + 1 + 1) & ~1;
   for (int v0 = 0; v0 < a.ncoef;) {
     const int left = a.ncoef - v0;
     const int nc = left >= 8 ? 8 : left >= 4 ? 4 : left >= 2 ? 2 : 1;
-    const long long n = ncols_total * nc;
-    series_gather_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
-        a.cols, ncols_total, a.c, a.ldc, v0, nc, cs);
+    // per-group stage: (K+1) x nj ChainCoef, nj AsmCoef, nj x 2nc row coefficients
+    const int buf_doubles = ((K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0) + nj * 2 * nc + 1) & ~1;
+    if (a.theta)
+      series_rowsum_kernel<true><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
+                                                           a.ldc, v0, nc, rowc);
+    else
+      series_rowsum_kernel<false><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
+                                                            a.ldc, v0, nc, rowc);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     switch (K) {
-      case 0: e = launch_ang<0>(a, cs, v0, nc, buf_doubles, st); break;
-      case 1: e = launch_ang<1>(a, cs, v0, nc, buf_doubles, st); break;
-      case 2: e = launch_ang<2>(a, cs, v0, nc, buf_doubles, st); break;
-      default: e = launch_ang<3>(a, cs, v0, nc, buf_doubles, st); break;
+      case 0: e = launch_ang<0>(a, rowc, v0, nc, buf_doubles, st); break;
+      case 1: e = launch_ang<1>(a, rowc, v0, nc, buf_doubles, st); break;
+      case 2: e = launch_ang<2>(a, rowc, v0, nc, buf_doubles, st); break;
+      default: e = launch_ang<3>(a, rowc, v0, nc, buf_doubles, st); break;
     }
     if (e != cudaSuccess) return e;
     *launches += 2;
