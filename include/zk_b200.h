@@ -23,6 +23,7 @@
  *   zk_series_eval                      <- new (B @ c; oracle numpy)
  *   zk_gram_accumulate                  <- new (B^T B, B^T y; nearest
  *                                          reference: tests/test_acceptance.py:150-172)
+ *   zk_direct_eval / zk_ztt_eval        <- zk/evaluate.py:189-247 float baselines
  *
  * Conventions
  *   - Every function returns int: ZK_OK (0) or a negative ZK_E* code; the
@@ -144,6 +145,20 @@ int zk_gram_accumulate(zk_ctx* ctx, const zk_plan* plan, const double* rho,
  * same expression tree and IEEE division). */
 int zk_jacobi_chain(zk_ctx* ctx, const double* x, int64_t N, int j_max, int alpha,
                     int beta, double* out, int64_t ldo, uint32_t flags);
+
+/* ---- the reference's float baselines on the GPU -----------
+ * zk_direct_eval  <- zk/evaluate.py:189-208 radial_direct: column c is the
+ *   polynomial sum_t coef[t] u^(T-t) (Horner in u = rho^2, coef[term_ptr[c] ..
+ *   term_ptr[c+1]) in descending order, exact integers rounded once) times
+ *   rho^low_exp[c]; an empty term range is the zero polynomial.
+ * zk_ztt_eval     <- zk/evaluate.py:211-247 radial_ztt_table: the Zernike
+ *   three-term recursion with rho^q seeds, columns (n, |m|), n <= 256.
+ * out is column-major P x M (ld >= P). */
+int zk_direct_eval(zk_ctx* ctx, const double* rho, int64_t P, const double* coef,
+                   const int32_t* term_ptr, const int32_t* low_exp, int64_t M, double* out,
+                   int64_t ld, uint32_t flags);
+int zk_ztt_eval(zk_ctx* ctx, const double* rho, int64_t P, const int32_t* mode_n,
+                const int32_t* mode_m, int64_t M, double* out, int64_t ld, uint32_t flags);
 
 /* ---- pinned host memory (for host-output pipelines at full PCIe rate) ---- */
 int zk_host_alloc(int64_t bytes, void** out);

@@ -329,3 +329,39 @@ def quad_table(modes, rho, k: int = 0) -> np.ndarray:
         if rc:
             raise ValueError("bad derivative order")
     return out.T
+
+
+# --------------------------------------------------------------------------
+# float baselines (zk/evaluate.py:189-247), for the GPU baseline kernels
+# --------------------------------------------------------------------------
+
+def direct_single(n: int, m_abs: int, rho, k: int = 0) -> np.ndarray:
+    """zk/evaluate.py:189-208: Horner in u = rho*rho over coefficients rounded
+    once to binary64, times rho**low."""
+    rho = np.atleast_1d(np.asarray(rho, dtype=np.float64))
+    terms = exact_terms(n, m_abs, k)
+    if not terms:
+        return np.zeros_like(rho)
+    u = rho * rho
+    acc = np.full_like(rho, float(terms[0][1]))
+    for _, c in terms[1:]:
+        acc = acc * u + float(c)
+    return acc * rho ** terms[-1][0]
+
+
+def ztt_table(modes, rho) -> np.ndarray:
+    """zk/evaluate.py:211-241: memoised Zernike three-term recursion."""
+    rho = np.atleast_1d(np.asarray(rho, dtype=np.float64))
+    memo: dict = {}
+
+    def level(n, m):
+        if (n, m) in memo:
+            return memo[(n, m)]
+        v = rho ** n if n == m else rho * (level(n - 1, abs(m - 1)) + level(n - 1, m + 1)) - level(n - 2, m)
+        memo[(n, m)] = v
+        return v
+
+    out = np.empty((rho.size, len(modes)), dtype=np.float64)
+    for c, (n, m) in enumerate(modes):
+        out[:, c] = level(int(n), abs(int(m)))
+    return out

@@ -8,6 +8,7 @@ come from hand-written sm_100a CUDA kernels behind the C ABI in
 (``paper_2409_19156_b200/lib/libzk_b200.so``); there is no CPU fallback.
 """
 
+from .baselines import radial_direct, radial_direct_table, radial_ztt, radial_ztt_table
 from .batch import (
     STRATEGIES,
     BatchRequest,
@@ -77,4 +78,5 @@ __all__ = [
     "rational_radial_grid", "zernike_basis", "zernike_eval", "zernike_radial",
     "series_eval", "series_device", "gram", "gram_device", "fit", "fit_sharded",
     "solve_normal", "allreduce_normal_equations", "shard_range", "radial_basis_shard",
+    "radial_direct", "radial_direct_table", "radial_ztt", "radial_ztt_table",
 ]

@@ -66,6 +66,10 @@ SIGNATURES = {
                                    c_void_p, c_void_p, c_void_p, c_uint32]),
     "zk_jacobi_chain": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int,
                                 c_void_p, c_int64, c_uint32]),
+    "zk_direct_eval": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                               c_int64, c_void_p, c_int64, c_uint32]),
+    "zk_ztt_eval": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64,
+                            c_void_p, c_int64, c_uint32]),
     "zk_host_alloc": (c_int, [c_int64, POINTER(c_void_p)]),
     "zk_host_free": (c_int, [c_void_p]),
 }

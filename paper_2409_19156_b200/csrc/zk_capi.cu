@@ -872,3 +872,119 @@ int zk_host_free(void* p) {
 }
 
 }  // extern "C"
+
+// Shared host/device staging for the small baseline kernels: inputs (rho and
+// the integer/coefficient tables) go to device scratch, the P x M result comes
+// back with one 2-D copy when the output is a host pointer.
+namespace {
+struct Staged {
+  const double* rho;
+  double* out;
+  int64_t ld;
+  char* tail;  // free scratch after rho/out for small tables
+};
+
+int stage_baseline(zk_ctx* ctx, const double* rho, int64_t P, int64_t M, double* out, int64_t ld,
+                   uint32_t flags, size_t extra, Staged& s) {
+  const bool host_in = (flags & ZK_HOST_INPUT) != 0;
+  const bool host_out = (flags & ZK_HOST_OUTPUT) != 0;
+  const size_t rb = align_up(size_t(P) * 8, 256);
+  const size_t ob = host_out ? align_up(size_t(P) * size_t(M) * 8, 256) : 0;
+  int rc = ensure_scratch(ctx, 0, rb + ob + align_up(extra, 256) + 256);
+  if (rc) return rc;
+  char* base = static_cast<char*>(ctx->scratch[0]);
+  s.rho = rho;
+  if (host_in) {
+    ZK_CUDA(cudaMemcpyAsync(base, rho, size_t(P) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    s.rho = reinterpret_cast<const double*>(base);
+  }
+  s.out = host_out ? reinterpret_cast<double*>(base + rb) : out;
+  s.ld = host_out ? P : ld;
+  s.tail = base + rb + ob;
+  return ZK_OK;
+}
+
+int finish_baseline(zk_ctx* ctx, int64_t P, int64_t M, double* out, int64_t ld, uint32_t flags,
+                    const Staged& s) {
+  if (flags & ZK_HOST_OUTPUT)
+    ZK_CUDA(cudaMemcpy2DAsync(out, size_t(ld) * 8, s.out, size_t(P) * 8, size_t(P) * 8, size_t(M),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+  ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ZK_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int zk_direct_eval(zk_ctx* ctx, const double* rho, int64_t P, const double* coef,
+                   const int32_t* term_ptr, const int32_t* low_exp, int64_t M, double* out,
+                   int64_t ld, uint32_t flags) {
+  if (!ctx) return fail(ZK_EINVAL, "null ctx");
+  if (P < 0 || M < 0 || ld < P) return fail(ZK_EINVAL, "bad sizes");
+  if (P == 0 || M == 0) return ZK_OK;
+  if (!rho || !out || !term_ptr || !low_exp) return fail(ZK_EINVAL, "null data pointer");
+  const int64_t T = term_ptr[M];
+  if (T < 0 || (T > 0 && !coef)) return fail(ZK_EINVAL, "bad term table");
+  for (int64_t c = 0; c < M; ++c)
+    if (term_ptr[c] > term_ptr[c + 1] || term_ptr[c] < 0 || low_exp[c] < 0)
+      return fail(ZK_EINVAL, "bad term table at column " + std::to_string(c));
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  ZK_CUDA(cudaSetDevice(ctx->device));
+  const size_t cb = align_up(size_t(T) * 8, 256), pb = align_up(size_t(M + 1) * 4, 256);
+  Staged s{};
+  int rc = stage_baseline(ctx, rho, P, M, out, ld, flags, cb + 2 * pb, s);
+  if (rc) return rc;
+  double* dcoef = reinterpret_cast<double*>(s.tail);
+  int32_t* dptr = reinterpret_cast<int32_t*>(s.tail + cb);
+  int32_t* dlow = reinterpret_cast<int32_t*>(s.tail + cb + pb);
+  // the term tables are host arrays (built from exact integers by the caller)
+  if (T) ZK_CUDA(cudaMemcpyAsync(dcoef, coef, size_t(T) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  ZK_CUDA(cudaMemcpyAsync(dptr, term_ptr, size_t(M + 1) * 4, cudaMemcpyHostToDevice, ctx->stream));
+  ZK_CUDA(cudaMemcpyAsync(dlow, low_exp, size_t(M) * 4, cudaMemcpyHostToDevice, ctx->stream));
+  ZK_CUDA(zk::launch_direct(s.rho, P, dcoef, dptr, dlow, M, s.out, s.ld, ctx->stream));
+  ctx->launches += 1;
+  return finish_baseline(ctx, P, M, out, ld, flags, s);
+}
+
+int zk_ztt_eval(zk_ctx* ctx, const double* rho, int64_t P, const int32_t* mode_n,
+                const int32_t* mode_m, int64_t M, double* out, int64_t ld, uint32_t flags) {
+  if (!ctx) return fail(ZK_EINVAL, "null ctx");
+  if (P < 0 || M < 0 || ld < P) return fail(ZK_EINVAL, "bad sizes");
+  if (P == 0 || M == 0) return ZK_OK;
+  if (!rho || !out || !mode_n || !mode_m) return fail(ZK_EINVAL, "null data pointer");
+  std::string err = zk::validate_modes(mode_n, mode_m, M);
+  if (!err.empty()) return fail(ZK_EINVAL, err);
+  int N = 0;
+  for (int64_t c = 0; c < M; ++c) N = std::max(N, mode_n[c]);
+  if (N > zk::ztt_max_degree())
+    return fail(ZK_EINVAL, "ztt baseline supports n <= " + std::to_string(zk::ztt_max_degree()));
+  // per level n: the (|m|, column) pairs to emit, in column order
+  std::vector<int32_t> ptr(static_cast<size_t>(N) + 2, 0);
+  std::vector<int32_t> lm(static_cast<size_t>(M)), lc(static_cast<size_t>(M));
+  for (int64_t c = 0; c < M; ++c) ptr[size_t(mode_n[c]) + 1]++;
+  for (int n = 0; n <= N; ++n) ptr[size_t(n) + 1] += ptr[size_t(n)];
+  std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
+  for (int64_t c = 0; c < M; ++c) {
+    const int32_t slot = fill[size_t(mode_n[c])]++;
+    lm[size_t(slot)] = std::abs(mode_m[c]);
+    lc[size_t(slot)] = static_cast<int32_t>(c);
+  }
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  ZK_CUDA(cudaSetDevice(ctx->device));
+  const size_t pb = align_up(ptr.size() * 4, 256), mb = align_up(size_t(M) * 4, 256);
+  Staged s{};
+  int rc = stage_baseline(ctx, rho, P, M, out, ld, flags, pb + 2 * mb, s);
+  if (rc) return rc;
+  int32_t* dptr = reinterpret_cast<int32_t*>(s.tail);
+  int32_t* dm = reinterpret_cast<int32_t*>(s.tail + pb);
+  int32_t* dc = reinterpret_cast<int32_t*>(s.tail + pb + mb);
+  ZK_CUDA(cudaMemcpyAsync(dptr, ptr.data(), ptr.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  ZK_CUDA(cudaMemcpyAsync(dm, lm.data(), size_t(M) * 4, cudaMemcpyHostToDevice, ctx->stream));
+  ZK_CUDA(cudaMemcpyAsync(dc, lc.data(), size_t(M) * 4, cudaMemcpyHostToDevice, ctx->stream));
+  ZK_CUDA(zk::launch_ztt(s.rho, P, N, dptr, dm, dc, s.out, s.ld, ctx->stream));
+  ctx->launches += 1;
+  // the host tables above are copied asynchronously: finish before they go out of scope
+  return finish_baseline(ctx, P, M, out, ld, flags, s);
+}
+
+}  // extern "C"

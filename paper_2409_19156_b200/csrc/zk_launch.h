@@ -67,4 +67,12 @@ cudaError_t launch_gram_panel(const double* panel, long long ld, long long kpane
 cudaError_t launch_chain(const double* x, long long N, int jmax, int alpha, int beta,
                          double* out, long long ldo, cudaStream_t st);
 
+cudaError_t launch_direct(const double* rho, long long P, const double* coef,
+                          const int32_t* term_ptr, const int32_t* low_exp, long long M,
+                          double* out, long long ld, cudaStream_t st);
+int ztt_max_degree();
+cudaError_t launch_ztt(const double* rho, long long P, int N, const int32_t* lvl_ptr,
+                       const int32_t* lvl_m, const int32_t* lvl_col, double* out, long long ld,
+                       cudaStream_t st);
+
 }  // namespace zk

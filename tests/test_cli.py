@@ -27,7 +27,7 @@ def test_usage_errors_exit_2(tmp_path):
     assert res.exit_code == 2
     res = CliRunner().invoke(main, ["bench", "--n-min", "5", "--n-max", "2"])
     assert res.exit_code == 2
-    res = CliRunner().invoke(main, ["bench", "--method", "direct"])
+    res = CliRunner().invoke(main, ["bench", "--method", "bogus"])
     assert res.exit_code == 2
 
 
@@ -75,6 +75,11 @@ def test_bench_records(tmp_path):
     assert tuple(rows[0]) == BENCH_HEADER
     assert len(rows) == 1 + 3 * 2
     by = {(r[1], int(r[2])): int(r[5]) for r in rows[1:]}
+    res = CliRunner().invoke(main, ["bench", "--n-min", "30", "--n-max", "30", "--grid-size", "100",
+                                    "--method", "jacobi", "--method", "direct", "--method", "ztt",
+                                    "--reps", "3", "--output", str(out)])
+    assert res.exit_code == 0, res.output
+    assert {r[0] for r in list(csv.reader(open(out)))[1:]} == {"jacobi", "direct", "ztt"}
     for n in (10, 20, 30):
         assert by[("cached", n)] <= by[("independent", n)]
         assert by[("cached", n)] == sum(max(0, (n - a) // 2 - 1) for a in range(n + 1))
