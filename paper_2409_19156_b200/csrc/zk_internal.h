@@ -11,7 +11,7 @@ namespace zk {
 // zk/evaluate.py:70-74 held exactly as binary64 plus the correctly rounded
 // reciprocal of `lead` (used for an exact, Markstein-corrected division).
 // Six doubles so a warp-uniform entry is three 16-byte shared-memory loads.
-struct ChainCoef {
+struct alignas(16) ChainCoef {
   double mid_x;      // (c-1) c (c-2)
   double mid_const;  // (c-1) (alpha^2 - beta^2)
   double last;       // 2 (j+alpha-1)(j+beta-1) c
@@ -23,7 +23,7 @@ static_assert(sizeof(ChainCoef) == 48, "ChainCoef layout");
 
 // Derivative prefactors per jacobi degree j of a group (zk/evaluate.py:127-149);
 // every product is an exact integer or half-integer in binary64.
-struct AsmCoef {
+struct alignas(16) AsmCoef {
   double c11;  // k=1: 4 s1
   double c21;  // k=2: 4 (2m+1) s1
   double c22;  // k=2: 16 s2

@@ -52,6 +52,35 @@ __device__ __forceinline__ dd dd_pow(double x, int e) {
   return r;
 }
 
+// Shared-memory coefficient loads as 16-byte vectors (three LDS.128 per chain
+// step instead of five scalar loads).
+__device__ __forceinline__ ChainCoef load_coef(const ChainCoef* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = q[0], b = q[1], c = q[2];
+  ChainCoef r;
+  r.mid_x = a.x;
+  r.mid_const = a.y;
+  r.last = b.x;
+  r.rcp_lead = b.y;
+  r.lead = c.x;
+  r.pad = c.y;
+  return r;
+}
+
+__device__ __forceinline__ AsmCoef load_asm(const AsmCoef* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = q[0], b = q[1], c = q[2];
+  AsmCoef r;
+  r.c11 = a.x;
+  r.c21 = a.y;
+  r.c22 = b.x;
+  r.c31 = b.y;
+  r.c32 = c.x;
+  r.c33 = c.y;
+  r.pad0 = r.pad1 = 0.0;
+  return r;
+}
+
 // u = 1 - (2 rho) rho   (zk/evaluate.py:33)
 __device__ __forceinline__ double jacobi_u(double rho) {
   return __dsub_rn(1.0, __dmul_rn(2.0 * rho, rho));

@@ -287,7 +287,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
       const int r_hi = s_row[j + 1];
       if (r_lo == r_hi) return;  // CTA-uniform
       AsmCoef ac;
-      if constexpr (K > 0) ac = s_asm[j];
+      if constexpr (K > 0) ac = load_asm(s_asm + j);
       double val[NO][VEC];
       th.template values<decltype(steady)::value>(j, ac, chs, val);
       if (!use_tma) {
@@ -356,7 +356,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
             th.cur[i][v] = jacobi_p1(a1, ab2, th.u[v]);
           }
         } else if (d >= 2) {
-          const ChainCoef c = s_coef[i * nj + d];
+          const ChainCoef c = load_coef(s_coef + i * nj + d);
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
             const double nx = jacobi_step(c, th.u[v], th.cur[i][v], th.prev[i][v]);
@@ -376,14 +376,14 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
     for (; j + 1 <= jmax; j += 2) {
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = s_coef[i * nj + (j - i)];
+        const ChainCoef c = load_coef(s_coef + i * nj + (j - i));
 #pragma unroll
         for (int v = 0; v < VEC; ++v) B[i][v] = jacobi_step(c, th.u[v], A[i][v], B[i][v]);
       }
       emit(j, B, std::true_type{});
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = s_coef[i * nj + (j + 1 - i)];
+        const ChainCoef c = load_coef(s_coef + i * nj + (j + 1 - i));
 #pragma unroll
         for (int v = 0; v < VEC; ++v) A[i][v] = jacobi_step(c, th.u[v], B[i][v], A[i][v]);
       }
@@ -392,7 +392,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
     if (j <= jmax) {
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = s_coef[i * nj + (j - i)];
+        const ChainCoef c = load_coef(s_coef + i * nj + (j - i));
 #pragma unroll
         for (int v = 0; v < VEC; ++v) B[i][v] = jacobi_step(c, th.u[v], A[i][v], B[i][v]);
       }

@@ -143,7 +143,7 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
     // fold degree j's value into the running sums; STEADY: all chains >= 2
     auto fold = [&](int j, const double(&chs)[K + 1][kVec], auto steady) {
       AsmCoef ac;
-      if constexpr (K > 0) ac = s_asm[j];
+      if constexpr (K > 0) ac = load_asm(s_asm + j);
       double val[kVec];
 #pragma unroll
       for (int v = 0; v < kVec; ++v) {
@@ -182,7 +182,7 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
             A[i][v] = jacobi_p1(a1, ab2, u[v]);
           }
         } else if (d >= 2) {
-          const ChainCoef c = s_coef[i * nj + d];
+          const ChainCoef c = load_coef(s_coef + i * nj + d);
 #pragma unroll
           for (int v = 0; v < kVec; ++v) {
             const double nx = jacobi_step(c, u[v], A[i][v], B[i][v]);
@@ -197,14 +197,14 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
     for (; j + 1 <= jmax; j += 2) {
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = s_coef[i * nj + (j - i)];
+        const ChainCoef c = load_coef(s_coef + i * nj + (j - i));
 #pragma unroll
         for (int v = 0; v < kVec; ++v) B[i][v] = jacobi_step(c, u[v], A[i][v], B[i][v]);
       }
       fold(j, B, std::true_type{});
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = s_coef[i * nj + (j + 1 - i)];
+        const ChainCoef c = load_coef(s_coef + i * nj + (j + 1 - i));
 #pragma unroll
         for (int v = 0; v < kVec; ++v) A[i][v] = jacobi_step(c, u[v], B[i][v], A[i][v]);
       }
@@ -213,7 +213,7 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
     if (j <= jmax) {
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = s_coef[i * nj + (j - i)];
+        const ChainCoef c = load_coef(s_coef + i * nj + (j - i));
 #pragma unroll
         for (int v = 0; v < kVec; ++v) B[i][v] = jacobi_step(c, u[v], A[i][v], B[i][v]);
       }
