@@ -433,10 +433,15 @@ radial_basis_kernel_3cta(const RadialArgs a) {
 
 template <int K, bool ALL, bool ANG, int VEC, bool TMA>
 static cudaError_t launch_t(const RadialArgs& a, int grid, size_t smem, cudaStream_t st) {
-  auto fn = (K == 3 && !TMA && VEC <= 2)
-                 ? (ALL ? radial_basis_kernel_2cta<K, ALL, ANG, VEC, TMA>
-                        : radial_basis_kernel_3cta<K, ALL, ANG, VEC, TMA>)
-                 : radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
+  void (*fn)(RadialArgs);
+  if constexpr (K == 3 && !TMA && VEC <= 2) {
+    if constexpr (ALL)
+      fn = radial_basis_kernel_2cta<K, ALL, ANG, VEC, TMA>;
+    else
+      fn = radial_basis_kernel_3cta<K, ALL, ANG, VEC, TMA>;
+  } else {
+    fn = radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
+  }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
