@@ -699,8 +699,14 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const do
     rc = ensure_scratch(ctx, 1, zk::series_scratch_bytes(nrowslots));
     if (rc) return rc;
     int launches = 0;
+    // several coefficient vectors make the series a dense contraction: DMMA path
+    const int dm = env_int("ZK_SERIES_DMMA", -1);
+    const int nch = zk::series_dmma_chunks(static_cast<int>(std::min<int64_t>(ncoef, 32)));
+    const bool dmma = (dm < 0 ? ncoef >= 8 : dm != 0) &&
+                      zk::series_dmma_smem_bytes(deriv_order, plan->host.max_jmax, nch) <=
+                          ctx->max_smem;
     cudaError_t e = zk::launch_series(a, deriv_order, plan->host.max_jmax, nrowslots,
-                                      static_cast<double*>(ctx->scratch[1]), st, &launches);
+                                      static_cast<double*>(ctx->scratch[1]), dmma, st, &launches);
     ctx->launches += launches;
     if (e != cudaSuccess) return cuda_fail(e, "series kernel launch");
   }

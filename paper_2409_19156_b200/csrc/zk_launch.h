@@ -56,7 +56,11 @@ struct SeriesArgs {
 
 size_t series_scratch_bytes(long long nrowslots);
 cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nrowslots,
-                          double* rowc, cudaStream_t st, int* launches);
+                          double* rowc, bool dmma, cudaStream_t st, int* launches);
+int series_dmma_chunks(int ncoef);
+size_t series_dmma_smem_bytes(int K, int max_jmax, int nch);
+cudaError_t launch_series_dmma(const SeriesArgs& a, int K, int nch, int v0, int nc, int max_jmax,
+                               const double* rowc, cudaStream_t st);
 
 size_t gram_smem_bytes();
 int gram_k_granule();  // points per SYRK pipeline step (panel rows are padded to it)

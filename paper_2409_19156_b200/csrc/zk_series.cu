@@ -45,25 +45,28 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }  // namespace
 
 // rowc[(row0 + j) * 2NC + 2v + {0,1}] = (-1)^j * (C+, C-) of key (alpha, j)
+// (vectors v >= nc of a stride-wide record are zero: DMMA pads to 8 vectors)
 template <bool ANG>
 __global__ void series_rowsum_kernel(const GroupRec* __restrict__ groups,
                                      const int32_t* __restrict__ rowptr,
                                      const int32_t* __restrict__ cols,
                                      const double* __restrict__ c, long long ldc, int v0, int nc,
-                                     double* __restrict__ rowc) {
+                                     int stride, double* __restrict__ rowc) {
   const GroupRec g = groups[blockIdx.x];
   for (int j = threadIdx.x; j <= g.jmax; j += blockDim.x) {
     const int r_lo = rowptr[g.row0 + j], r_hi = rowptr[g.row0 + j + 1];
     const double sgn = (j & 1) ? -1.0 : 1.0;
-    for (int v = 0; v < nc; ++v) {
+    for (int v = 0; v < stride; ++v) {
       double cp = 0.0, cn = 0.0;
-      for (int r = r_lo; r < r_hi; ++r) {
-        const int code = cols[r];
-        const double x = c[(code >> 1) + static_cast<long long>(v0 + v) * ldc];
-        if (ANG && (code & 1)) cn += x; else cp += x;
+      if (v < nc) {
+        for (int r = r_lo; r < r_hi; ++r) {
+          const int code = cols[r];
+          const double x = c[(code >> 1) + static_cast<long long>(v0 + v) * ldc];
+          if (ANG && (code & 1)) cn += x; else cp += x;
+        }
       }
-      rowc[(static_cast<long long>(g.row0) + j) * 2 * nc + 2 * v] = sgn * cp;
-      rowc[(static_cast<long long>(g.row0) + j) * 2 * nc + 2 * v + 1] = sgn * cn;
+      rowc[(static_cast<long long>(g.row0) + j) * 2 * stride + 2 * v] = sgn * cp;
+      rowc[(static_cast<long long>(g.row0) + j) * 2 * stride + 2 * v + 1] = sgn * cn;
     }
   }
 }
@@ -261,14 +264,32 @@ static cudaError_t launch_ang(const SeriesArgs& a, const double* rowc, int v0, i
 }
 
 size_t series_scratch_bytes(long long nrowslots) {
-  return static_cast<size_t>(nrowslots) * 2 * 8 * sizeof(double) + 256;
+  return static_cast<size_t>(nrowslots) * 2 * 32 * sizeof(double) + 256;
 }
 
 cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nrowslots,
-                          double* rowc, cudaStream_t st, int* launches) {
+                          double* rowc, bool dmma, cudaStream_t st, int* launches) {
   (void)nrowslots;
   if (a.P <= 0) return cudaSuccess;
   const int nj = max_jmax + 1;
+  if (dmma) {  // tensor-core path: up to 32 vectors per launch, zero-padded to 8s
+    const int nch = series_dmma_chunks(a.ncoef);
+    const int per = 8 * nch;
+    for (int v0 = 0; v0 < a.ncoef; v0 += per) {
+      const int nc = a.ncoef - v0 < per ? a.ncoef - v0 : per;
+      if (a.theta)
+        series_rowsum_kernel<true><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
+                                                             a.ldc, v0, nc, per, rowc);
+      else
+        series_rowsum_kernel<false><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
+                                                              a.ldc, v0, nc, per, rowc);
+      cudaError_t e = cudaGetLastError();
+      if (e == cudaSuccess) e = launch_series_dmma(a, K, nch, v0, nc, max_jmax, rowc, st);
+      if (e != cudaSuccess) return e;
+      *launches += 2;
+    }
+    return cudaSuccess;
+  }
   for (int v0 = 0; v0 < a.ncoef;) {
     const int left = a.ncoef - v0;
     const int nc = left >= 8 ? 8 : left >= 4 ? 4 : left >= 2 ? 2 : 1;
@@ -276,10 +297,10 @@ cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nr
     const int buf_doubles = ((K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0) + nj * 2 * nc + 1) & ~1;
     if (a.theta)
       series_rowsum_kernel<true><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
-                                                           a.ldc, v0, nc, rowc);
+                                                           a.ldc, v0, nc, nc, rowc);
     else
       series_rowsum_kernel<false><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
-                                                            a.ldc, v0, nc, rowc);
+                                                            a.ldc, v0, nc, nc, rowc);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     switch (K) {

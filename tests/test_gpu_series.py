@@ -113,3 +113,22 @@ def test_device_accumulate_equals_single_call():
     assert np.abs(x.cpu().numpy() - np.linalg.solve(Gh, rh)).max() < 1e-8
     f = zb.series_device(modes, x, t(rho), t(theta))
     assert f.shape == (4096,)
+
+
+@pytest.mark.parametrize("path", ["0", "1"])
+@pytest.mark.parametrize("k", [0, 2])
+@pytest.mark.parametrize("V", [1, 5, 8, 13])
+def test_series_fma_and_dmma_paths(monkeypatch, path, k, V):
+    """Both series engines (per-key FMA folding, and the DMMA contraction
+    used for several coefficient vectors) against B @ C, 2-D and radial."""
+    monkeypatch.setenv("ZK_SERIES_DMMA", path)
+    modes = zb.full_mode_set(23)
+    pairs = [(md.n, md.m) for md in modes]
+    rho, theta = disc(1000, V + 7 * k)
+    C = np.random.default_rng(V).standard_normal((len(modes), V))
+    for th in (theta, None):
+        f = zb.series_eval(modes, C, rho, th, k)
+        B = orc.basis_2d(pairs, rho, theta, k) if th is not None else orc.radial_batch(pairs, rho, k)
+        ref = B @ C
+        scale = np.abs(B) @ np.abs(C)
+        assert (np.abs(f - ref) <= 1e-13 * scale + 1e-13).all(), (path, k, V, th is None)
