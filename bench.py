@@ -191,10 +191,15 @@ def run_gpu(args, world, rank, local):
     modes = zb.full_mode_set(N_RES)
     n_arr, m_arr = zb.modes.mode_arrays(modes)
     M = len(modes)
-    P = P_PER_GPU
-    Pg = P * world
+    if args.scaling == "strong":  # config 2 as stated: 1e5 points split over the ranks
+        Pg = P_PER_GPU
+        lo, hi = zb.shard_range(Pg, world, rank)
+    else:  # weak: 1e5 points per rank, the global grid grows with the world
+        Pg = P_PER_GPU * world
+        lo, hi = rank * P_PER_GPU, (rank + 1) * P_PER_GPU
+    P = hi - lo
     grid_global = zb.linear_radial_grid(Pg)
-    shard = np.ascontiguousarray(grid_global[rank * P:(rank + 1) * P])
+    shard = np.ascontiguousarray(grid_global[lo:hi])
 
     ctx = _lib.context(local)
     plan = _lib.plan_for(ctx, n_arr, m_arr)
@@ -236,7 +241,7 @@ def run_gpu(args, world, rank, local):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
     ms_per_step = t_ms / args.steps
-    value = world * P * M / (ms_per_step * 1e-3)
+    value = Pg * M / (ms_per_step * 1e-3)  # every rank's points / max-over-ranks time
 
     # ---- roofline of the dominant (only) kernel: algorithmic bytes per launch
     alg_bytes = 8.0 * P * M + 8.0 * P  # basis writes + grid reads
@@ -288,7 +293,7 @@ def run_gpu(args, world, rank, local):
         e2e_ok = bool(np.array_equal(host_view[:P], out[0].cpu().numpy()))
         _lib.lib.zk_host_free(hbuf)
         _lib.lib.zk_host_free(rbuf)
-        e2e = {"value": world * P * M / te, "unit": UNIT, "h2d_bytes_per_step": 8 * P,
+        e2e = {"value": Pg * M / te, "unit": UNIT, "h2d_bytes_per_step": 8 * P,
                "d2h_bytes_per_step": 8 * P * M, "ms_per_step": te * 1e3,
                "path": "zk_radial_eval(ZK_HOST_INPUT|ZK_HOST_OUTPUT), pinned host buffers, "
                        "chunked 2-stream D2H pipeline", "matches_device": e2e_ok}
@@ -308,7 +313,7 @@ def run_gpu(args, world, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"full mode set n<={N_RES} ({M} modes) x {P} radial points per GPU "
                                f"(linear grid i/(P-1), global {Pg} points sharded), k=0",
@@ -341,6 +346,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: 1e5 points per GPU (default); strong: 1e5 points in total")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
