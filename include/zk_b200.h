@@ -24,6 +24,7 @@
  *   zk_gram_accumulate                  <- new (B^T B, B^T y; nearest
  *                                          reference: tests/test_acceptance.py:150-172)
  *   zk_direct_eval / zk_ztt_eval        <- zk/evaluate.py:189-247 float baselines
+ *   zk_radial_eval_dd                   <- zk/exact.py:129-169 oracle_table (accuracy study)
  *
  * Conventions
  *   - Every function returns int: ZK_OK (0) or a negative ZK_E* code; the
@@ -159,6 +160,15 @@ int zk_direct_eval(zk_ctx* ctx, const double* rho, int64_t P, const double* coef
                    int64_t ld, uint32_t flags);
 int zk_ztt_eval(zk_ctx* ctx, const double* rho, int64_t P, const int32_t* mode_n,
                 const int32_t* mode_m, int64_t M, double* out, int64_t ld, uint32_t flags);
+
+/* ---- double-double reference values (GPU accuracy oracle) ---
+ * The K1 recursion/assembly in double-double arithmetic at double-double
+ * points (rho_hi + rho_lo, e.g. the exact rationals i/(P-1) of the
+ * reference's accuracy study), rounded once to binary64; stands in for
+ * zk/exact.py:129-169 oracle_table. rho_lo may be NULL. */
+int zk_radial_eval_dd(zk_ctx* ctx, const zk_plan* plan, const double* rho_hi,
+                      const double* rho_lo, int64_t P, int deriv_order, double* out, int64_t ld,
+                      uint32_t flags);
 
 /* ---- pinned host memory (for host-output pipelines at full PCIe rate) ---- */
 int zk_host_alloc(int64_t bytes, void** out);

@@ -258,6 +258,27 @@ def exact_value(terms, rho: float) -> float:
     return num / b ** top
 
 
+def exact_table_rational(modes, points, k: int = 0) -> np.ndarray:
+    """exact_table at exact rationals (fractions.Fraction), like the
+    reference's accuracy study (zk/cli.py:117-121)."""
+    out = np.empty((len(points), len(modes)), dtype=np.float64)
+    for col, (n, m) in enumerate(modes):
+        t = exact_terms(int(n), abs(int(m)), k)
+        for i, p in enumerate(points):
+            if not t:
+                out[i, col] = 0.0
+                continue
+            a, b = p.numerator, p.denominator
+            top, acc, bpow, prev = t[0][0], t[0][1], 1, t[0][0]
+            for e, c in t[1:]:
+                bpow *= b ** (prev - e)
+                acc = acc * a ** (prev - e) + c * bpow
+                prev = e
+            num = acc * a ** prev
+            out[i, col] = 0.0 if num == 0 else num / b ** top
+    return out
+
+
 def exact_table(modes, rho, k: int = 0) -> np.ndarray:
     """zk/exact.py:129-169: correctly rounded exact values, (P, M)."""
     pts = [float(x) for x in np.atleast_1d(np.asarray(rho, dtype=np.float64))]

@@ -8,6 +8,7 @@ come from hand-written sm_100a CUDA kernels behind the C ABI in
 (``paper_2409_19156_b200/lib/libzk_b200.so``); there is no CPU fallback.
 """
 
+from . import accuracy
 from .baselines import radial_direct, radial_direct_table, radial_ztt, radial_ztt_table
 from .batch import (
     STRATEGIES,

@@ -70,6 +70,8 @@ SIGNATURES = {
                                c_int64, c_void_p, c_int64, c_uint32]),
     "zk_ztt_eval": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64,
                             c_void_p, c_int64, c_uint32]),
+    "zk_radial_eval_dd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int,
+                                  c_void_p, c_int64, c_uint32]),
     "zk_host_alloc": (c_int, [c_int64, POINTER(c_void_p)]),
     "zk_host_free": (c_int, [c_void_p]),
 }

@@ -994,3 +994,32 @@ int zk_ztt_eval(zk_ctx* ctx, const double* rho, int64_t P, const int32_t* mode_n
 }
 
 }  // extern "C"
+
+extern "C" int zk_radial_eval_dd(zk_ctx* ctx, const zk_plan* plan, const double* rho_hi,
+                                 const double* rho_lo, int64_t P, int deriv_order, double* out,
+                                 int64_t ld, uint32_t flags) {
+  if (!ctx || !plan) return fail(ZK_EINVAL, "null ctx or plan");
+  if (plan->ctx != ctx) return fail(ZK_EINVAL, "plan belongs to another context");
+  if (deriv_order < 0 || deriv_order > plan->host.max_order)
+    return fail(ZK_EINVAL, "derivative order must be 0..3, got " + std::to_string(deriv_order));
+  const int64_t M = plan->host.M;
+  if (P < 0 || ld < P) return fail(ZK_EINVAL, "bad sizes");
+  if (P == 0 || M == 0) return ZK_OK;
+  if (!rho_hi || !out) return fail(ZK_EINVAL, "null data pointer");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  ZK_CUDA(cudaSetDevice(ctx->device));
+  Staged s{};
+  const size_t rb = align_up(size_t(P) * 8, 256);
+  int rc = stage_baseline(ctx, rho_hi, P, M, out, ld, flags, rb, s);
+  if (rc) return rc;
+  const double* lo = rho_lo;
+  if (rho_lo && (flags & ZK_HOST_INPUT)) {
+    ZK_CUDA(cudaMemcpyAsync(s.tail, rho_lo, size_t(P) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    lo = reinterpret_cast<const double*>(s.tail);
+  }
+  ZK_CUDA(zk::launch_radial_dd(plan->groups, static_cast<int>(plan->host.groups.size()),
+                               plan->rowptr, plan->cols, s.rho, lo, P, deriv_order, s.out, s.ld,
+                               ctx->stream));
+  ctx->launches += 1;
+  return finish_baseline(ctx, P, M, out, ld, flags, s);
+}

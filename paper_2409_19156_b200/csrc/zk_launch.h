@@ -79,4 +79,8 @@ cudaError_t launch_ztt(const double* rho, long long P, int N, const int32_t* lvl
                        const int32_t* lvl_m, const int32_t* lvl_col, double* out, long long ld,
                        cudaStream_t st);
 
+cudaError_t launch_radial_dd(const GroupRec* groups, int ngroups, const int32_t* rowptr,
+                             const int32_t* cols, const double* rho_hi, const double* rho_lo,
+                             long long P, int K, double* out, long long ld, cudaStream_t st);
+
 }  // namespace zk

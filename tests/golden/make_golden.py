@@ -143,6 +143,13 @@ def main():
             g[f"idx_req{r}_k{k}"] = vals
     g["idx_req_grid"] = zk.linear_radial_grid(33)
 
+    # ---- the reference's accuracy study (zk/cli.py:98-130), all methods, k <= 1
+    from zernkit.cli import METHODS, run_accuracy
+    rows = run_accuracy(24, METHODS, 100, 1, serial=True)
+    g["acc_rows"] = np.array([(r.n, r.m, r.deriv_order, METHODS.index(r.method)) for r in rows],
+                             dtype=np.int32)
+    g["acc_err"] = np.array([r.max_abs_err for r in rows])
+
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, os.path.getsize(OUT), "bytes;", len(g), "arrays")
 

@@ -65,6 +65,37 @@ def test_eval_csv_and_json_match_oracle(tmp_path):
     assert np.abs(np.array(payload["values"]) - ref2).max() <= 1e-13
 
 
+def test_accuracy_usage_errors():
+    res = CliRunner().invoke(main, ["accuracy", "--n-max", "151"])  # zk/cli.py:40 guard
+    assert res.exit_code == 2
+
+
+@pytest.mark.gpu
+def test_accuracy_matches_reference_study(golden, tmp_path):
+    """The reference's own accuracy CSV (golden: zernkit run_accuracy(24, all
+    methods, 100 points, k<=1) with the exact oracle) against ours (GPU
+    methods, double-double reference): same rows; the errors are mostly
+    identical and otherwise differ by an ulp of the evaluated value (rho**m
+    rounding), far below the north_star tolerance."""
+    out = tmp_path / "acc.csv"
+    res = CliRunner().invoke(main, ["accuracy", "--n-max", "24", "--k-max", "1",
+                                    "--output", str(out)])
+    assert res.exit_code == 0, res.output
+    rows = list(csv.reader(open(out)))
+    assert tuple(rows[0]) == ("n", "m", "k", "method", "max_abs_err")
+    meth = ("jacobi", "direct", "ztt")
+    got = [(int(r[0]), int(r[1]), int(r[2]), meth.index(r[3])) for r in rows[1:]]
+    assert np.array_equal(np.array(got, np.int32), golden["acc_rows"])
+    err = np.array([float(r[4]) for r in rows[1:]])
+    ref = golden["acc_err"]
+    for mi in (0, 2):  # ztt seeds are rho**q: every pow rounding shows up there
+        sel = golden["acc_rows"][:, 3] == mi
+        assert np.mean(err[sel] == ref[sel]) > (0.9 if mi == 0 else 0.5), meth[mi]
+        assert np.abs(err[sel] - ref[sel]).max() <= 1e-13, meth[mi]
+    sel = golden["acc_rows"][:, 3] == 1  # direct sum: same Horner arithmetic; rho**low rounding
+    assert np.abs(err[sel] - ref[sel]).max() <= 1e-13 + 0.05 * ref[sel].max()
+
+
 @pytest.mark.gpu
 def test_bench_records(tmp_path):
     out = tmp_path / "b.csv"

@@ -60,3 +60,25 @@ def test_baseline_validation():
         zb.radial_ztt_table(zb.full_mode_set(2), [1.5])
     with pytest.raises(ValueError):
         zb.radial_ztt_table(zb.as_mode_set([(300, 0)]), [0.5])  # beyond the kernel's degree cap
+
+
+def test_double_double_reference_equals_exact_oracle(golden):
+    """zk_radial_eval_dd (the GPU accuracy reference) reproduces the exact
+    oracle: on the golden n=200 binary64 points, and -- every order -- at the
+    exact rationals i/40 the reference's accuracy study uses."""
+    from fractions import Fraction
+
+    from paper_2409_19156_b200.accuracy import rational_grid_dd, reference_table
+    modes = zb.full_mode_set(200)
+    umodes = zb.as_mode_set([(modes[c].n, modes[c].m) for c in golden["c4_ucols"]])
+    got = reference_table(umodes, golden["c4_grid"], None, 0)
+    assert np.mean(got == golden["c4_exact"]) > 0.999
+    assert np.abs(got - golden["c4_exact"]).max() <= 1e-15 * np.abs(golden["c4_exact"]).max()
+    hi, lo = rational_grid_dd(41)
+    small = [(n, m) for n in range(31) for m in range(n % 2, n + 1, 2)]
+    pts = [Fraction(i, 40) for i in range(41)]
+    for k in range(4):
+        ref = reference_table(zb.as_mode_set(small), hi, lo, k)
+        ex = orc.exact_table_rational(small, pts, k)
+        assert np.mean(ref == ex) > 0.99, k
+        assert np.abs(ref - ex).max() <= 1e-14 * max(1.0, np.abs(ex).max()), k
