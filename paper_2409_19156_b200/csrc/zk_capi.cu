@@ -149,6 +149,8 @@ namespace {
 int ensure_scratch(zk_ctx* ctx, int slot, size_t bytes) {
   if (ctx->scratch_bytes[slot] >= bytes) return ZK_OK;
   if (ctx->scratch[slot]) {
+    // asynchronous calls (ZK_ASYNC) may still be using it on either stream
+    cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->pipe[slot]);
     cudaFree(ctx->scratch[slot]);
     ctx->scratch[slot] = nullptr;
