@@ -417,3 +417,27 @@ def test_mode_set_too_large_fails_loudly():
     modes = zb.as_mode_set([(6000, 0)])
     with pytest.raises(ValueError):
         radial(modes, [0.5], 3)
+
+
+@pytest.mark.parametrize("vec", ["4", "2", "1"])
+def test_store_paths_agree_bitwise(monkeypatch, vec):
+    """Every store path (32/16/8-byte direct stores; the TMA bulk-store ring
+    staged through shared memory) writes the same bits, including partial
+    tiles, all-orders strides and the 2-D basis."""
+    modes = zb.full_mode_set(40)
+    grid = np.random.default_rng(13).uniform(size=5003)  # partial last tile
+    th = np.random.default_rng(14).uniform(-3, 3, size=5003)
+    n = np.array([md.n for md in modes])
+    m = np.array([md.m for md in modes])
+    monkeypatch.setenv("ZK_VEC", vec)
+    monkeypatch.setenv("ZK_TMA", "0")
+    base = zb.evaluate_batch_all_orders(zb.BatchRequest(modes=modes, grid=grid, deriv_order=3))
+    base2d = zb.zernike_basis(grid, th, n, m)
+    monkeypatch.setenv("ZK_TMA", "1")
+    tma = zb.evaluate_batch_all_orders(zb.BatchRequest(modes=modes, grid=grid, deriv_order=3))
+    tma2d = zb.zernike_basis(grid, th, n, m)
+    for a, b in zip(base, tma):
+        assert np.array_equal(a.values, b.values)
+    assert np.array_equal(base2d, tma2d)
+    ref = orc.radial_batch(pairs(modes), grid[:64], 3)
+    assert within_tolerance(base[3].values[:64], ref)
