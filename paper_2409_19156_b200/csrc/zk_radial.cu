@@ -36,8 +36,14 @@ namespace zk {
 namespace {
 
 constexpr int kComputeWarps = kRadialThreads / 32;
-constexpr int kRingStages = 4;  // TMA staging ring depth
-constexpr int kRingLag = 1;     // bulk groups the producer keeps in flight before releasing
+#ifndef ZK_RING_STAGES
+#define ZK_RING_STAGES 4
+#endif
+#ifndef ZK_RING_LAG
+#define ZK_RING_LAG 1
+#endif
+constexpr int kRingStages = ZK_RING_STAGES;  // TMA staging ring depth
+constexpr int kRingLag = ZK_RING_LAG;        // bulk groups in flight before a stage is released
 
 // L2 policy for the basis stream: evict-first. The output is written once and
 // never re-read by this kernel; marking it evict-first lets L2 drain it to HBM
@@ -338,9 +344,12 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
       }
     };
 
-    // ---- prologue degrees: chain i at degree d = j - i may be 0 or 1
-    const int j_pro = min(jmax, K + 1);
-    for (int j = 0; j <= j_pro; ++j) {
+    // ---- prologue degrees: chain i at degree d = j - i may be 0 or 1. Fully
+    // unrolled (j is a compile-time constant), so every d-branch resolves
+    // statically.
+#pragma unroll
+    for (int j = 0; j <= K + 1; ++j) {
+      if (j > jmax) break;
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
         const int d = j - i;
@@ -418,9 +427,9 @@ radial_basis_kernel_2cta(const RadialArgs a) {
   radial_basis_body<K, ALL, ANG, VEC, TMA>(a);
 }
 
-// k = 3, one order: three CTAs per SM (85 registers, a few prologue spills)
-// measured 3 % faster than two; the all-orders variant is store-bound and
-// slower at three (more spills in its epilogue), so it keeps two.
+// k = 2, 3, one order: three CTAs per SM (85 registers, a few prologue
+// spills) measured faster than two; the k = 3 all-orders variant is
+// store-bound and slower at three (more spills in its epilogue), so it keeps two.
 template <int K, bool ALL, bool ANG, int VEC, bool TMA>
 __global__ void __launch_bounds__(kRadialThreads + (TMA ? 32 : 0), 3)
 radial_basis_kernel_3cta(const RadialArgs a) {
@@ -434,11 +443,10 @@ radial_basis_kernel_3cta(const RadialArgs a) {
 template <int K, bool ALL, bool ANG, int VEC, bool TMA>
 static cudaError_t launch_t(const RadialArgs& a, int grid, size_t smem, cudaStream_t st) {
   void (*fn)(RadialArgs);
-  if constexpr (K == 3 && !TMA && VEC <= 2) {
-    if constexpr (ALL)
-      fn = radial_basis_kernel_2cta<K, ALL, ANG, VEC, TMA>;
-    else
-      fn = radial_basis_kernel_3cta<K, ALL, ANG, VEC, TMA>;
+  if constexpr (K == 3 && !TMA && VEC <= 2 && ALL) {
+    fn = radial_basis_kernel_2cta<K, ALL, ANG, VEC, TMA>;
+  } else if constexpr (K >= 2 && !TMA && VEC <= 2 && !ALL) {
+    fn = radial_basis_kernel_3cta<K, ALL, ANG, VEC, TMA>;
   } else {
     fn = radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
   }
