@@ -168,8 +168,9 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
     };
 
     double A[K + 1][kVec], B[K + 1][kVec];  // A: newest degree, B: the one before
-    const int j_pro = min(jmax, K + 1);
-    for (int j = 0; j <= j_pro; ++j) {
+#pragma unroll
+    for (int j = 0; j <= K + 1; ++j) {  // prologue degrees, d-branches resolved at compile time
+      if (j > jmax) break;
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
         const int d = j - i;

@@ -123,8 +123,9 @@ series_dmma_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, 
       s_R[j * kLdp + tid] = assemble<K, K>(pw, ac, ch);
     };
     double A[K + 1], B[K + 1];
-    const int j_pro = min(jmax, K + 1);
-    for (int j = 0; j <= j_pro; ++j) {
+#pragma unroll
+    for (int j = 0; j <= K + 1; ++j) {  // prologue degrees, d-branches resolved at compile time
+      if (j > jmax) break;
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
         const int d = j - i;
