@@ -6,9 +6,11 @@ equal and whose only observable difference is the StepCounter. Here both
 strategies run the single fused kernel K1 (one sweep per (point, alpha)),
 so their values are bitwise equal by construction; each returns the
 reference's analytic counter for its strategy (zk/batch.py:69-94), computed
-by the native planner. ``parallel`` maps to nothing: the GPU grid replaces
-the reference's thread pool (zk/batch.py:136-141,174-180), and results are
-independent of it, as the reference requires (tests/test_batch.py:132-143).
+by the native planner. ``parallel=True`` spreads the points over every
+visible GPU (contiguous shards, one host thread per device, no communication;
+the reference's thread pool, zk/batch.py:136-141,174-180, becomes device
+parallelism); results are bitwise independent of it, as the reference
+requires (tests/test_batch.py:132-143).
 """
 
 from __future__ import annotations
@@ -18,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .evaluate import MAX_DERIV_ORDER, basis_matrix
+from .evaluate import MAX_DERIV_ORDER, basis_matrix, parallel_devices
 from .modes import DedupPlan, ModeSet, as_mode_set, mode_arrays
 from .tables import EvalMatrix, radial_grid
 
@@ -77,9 +79,11 @@ def independent_step_counter(plan: DedupPlan, deriv_order: int) -> StepCounter:
     return StepCounter(steps, chains)
 
 
-def _evaluate(request: BatchRequest, shared: bool) -> tuple[EvalMatrix, StepCounter]:
+def _evaluate(request: BatchRequest, shared: bool,
+              parallel: bool = False) -> tuple[EvalMatrix, StepCounter]:
     n, m = mode_arrays(request.modes)
-    values = basis_matrix(n, m, request.grid, request.deriv_order)
+    devices = parallel_devices() if parallel else None
+    values = basis_matrix(n, m, request.grid, request.deriv_order, devices=devices)
     table = EvalMatrix(values=values, modes=request.modes, deriv_order=request.deriv_order)
     return table, _counter(request.modes, request.deriv_order, shared)
 
@@ -88,7 +92,7 @@ def batch_cached(request: BatchRequest, parallel: bool = False) -> tuple[EvalMat
     """zk/batch.py:104-142."""
     if request.strategy != "cached":
         raise ValueError(f"request strategy is {request.strategy!r}, expected 'cached'")
-    return _evaluate(request, shared=True)
+    return _evaluate(request, shared=True, parallel=parallel)
 
 
 def batch_independent(request: BatchRequest,
@@ -97,7 +101,7 @@ def batch_independent(request: BatchRequest,
     if request.strategy != "independent":
         raise ValueError(
             f"request strategy is {request.strategy!r}, expected 'independent'")
-    return _evaluate(request, shared=False)
+    return _evaluate(request, shared=False, parallel=parallel)
 
 
 def evaluate_batch(request: BatchRequest,

@@ -75,30 +75,61 @@ def jacobi_chain(j_max: int, alpha: int, beta: int, x) -> np.ndarray:
     return out
 
 
+def parallel_devices() -> list[int]:
+    """Devices ``parallel=True`` spreads a host-level call over: ZK_DEVICES
+    (comma list) if set, else every visible GPU."""
+    import ctypes
+    import os
+    env = os.environ.get("ZK_DEVICES")
+    if env:
+        return [int(x) for x in env.split(",") if x.strip()]
+    cnt = ctypes.c_int(0)
+    _lib.check(_lib.lib.zk_device_count(ctypes.byref(cnt)), "zk_device_count")
+    return list(range(max(1, cnt.value)))
+
+
 def basis_matrix(mode_n: np.ndarray, mode_m: np.ndarray, rho: np.ndarray, k: int,
                  theta: np.ndarray | None = None, all_orders: bool = False,
-                 device: int | None = None):
+                 device: int | None = None, devices: list[int] | None = None):
     """Run K1 (theta None) or K1+K2 on host arrays; returns the (P, M)
     F-ordered matrix, or a list of k+1 of them when ``all_orders``.
-    Inputs must already be validated."""
+    ``devices``: split the points into contiguous shards, one per listed GPU,
+    each written straight into its rows of the shared result (one host thread
+    per device; the C ABI releases the GIL). Inputs must already be validated."""
     rho = np.ascontiguousarray(rho, dtype=np.float64)
     P, M = rho.size, int(np.asarray(mode_n).size)
     n_out = k + 1 if (all_orders and k > 0) else 1
     flat = np.empty(n_out * P * M, dtype=np.float64)
     mats = [flat[o * P * M:(o + 1) * P * M].reshape((P, M), order="F") for o in range(n_out)]
+    if theta is not None:
+        theta = np.ascontiguousarray(theta, dtype=np.float64)
+    devs = list(devices) if devices else [device]
     if P and M:
-        ctx = _lib.context(device)
-        plan = _lib.plan_for(ctx, mode_n, mode_m)
-        if theta is None:
-            rc = _lib.lib.zk_radial_eval(ctx.handle, plan.handle, _lib.dptr(rho), P, k,
-                                         int(n_out > 1), _lib.dptr(flat), P, P * M, _HOST)
-            _lib.check(rc, "zk_radial_eval")
+        from .sharding import shard_range
+
+        def run(shard: int):
+            lo, hi = shard_range(P, len(devs), shard)
+            if hi <= lo:
+                return
+            ctx = _lib.context(devs[shard])
+            plan = _lib.plan_for(ctx, mode_n, mode_m)
+            base = flat.ctypes.data + 8 * lo
+            if theta is None:
+                rc = _lib.lib.zk_radial_eval(ctx.handle, plan.handle, rho.ctypes.data + 8 * lo,
+                                             hi - lo, k, int(n_out > 1), base, P, P * M, _HOST)
+                _lib.check(rc, "zk_radial_eval")
+            else:
+                rc = _lib.lib.zk_zernike_eval(ctx.handle, plan.handle, rho.ctypes.data + 8 * lo,
+                                              theta.ctypes.data + 8 * lo, hi - lo, k,
+                                              int(n_out > 1), base, P, P * M, _HOST)
+                _lib.check(rc, "zk_zernike_eval")
+
+        if len(devs) == 1:
+            run(0)
         else:
-            theta = np.ascontiguousarray(theta, dtype=np.float64)
-            rc = _lib.lib.zk_zernike_eval(ctx.handle, plan.handle, _lib.dptr(rho),
-                                          _lib.dptr(theta), P, k, int(n_out > 1),
-                                          _lib.dptr(flat), P, P * M, _HOST)
-            _lib.check(rc, "zk_zernike_eval")
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(len(devs)) as pool:
+                list(pool.map(run, range(len(devs))))
     return mats if all_orders else mats[0]
 
 

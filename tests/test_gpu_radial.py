@@ -441,3 +441,25 @@ def test_store_paths_agree_bitwise(monkeypatch, vec):
     assert np.array_equal(base2d, tma2d)
     ref = orc.radial_batch(pairs(modes), grid[:64], 3)
     assert within_tolerance(base[3].values[:64], ref)
+
+
+def test_parallel_shards_over_devices_bitwise(monkeypatch):
+    """parallel=True splits the points across devices (here: two shards on
+    the one available GPU via ZK_DEVICES=0,0); every shard writes its rows of
+    the shared F-ordered result and the values are bitwise the serial ones."""
+    modes = zb.full_mode_set(25)
+    grid = np.random.default_rng(15).uniform(size=7777)
+    req = zb.BatchRequest(modes=modes, grid=grid, deriv_order=2)
+    serial, cs = zb.batch_cached(req)
+    monkeypatch.setenv("ZK_DEVICES", "0,0,0")
+    par, cp = zb.batch_cached(req, parallel=True)
+    assert np.array_equal(serial.values, par.values) and cs == cp
+    n = np.array([md.n for md in modes])
+    m = np.array([md.m for md in modes])
+    th = np.random.default_rng(16).uniform(size=7777)
+    from paper_2409_19156_b200.evaluate import basis_matrix
+    a = basis_matrix(n.astype(np.int32), m.astype(np.int32), grid, 1, theta=th, all_orders=True)
+    b = basis_matrix(n.astype(np.int32), m.astype(np.int32), grid, 1, theta=th, all_orders=True,
+                     devices=[0, 0])
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
