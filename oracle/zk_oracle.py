@@ -23,6 +23,7 @@ from __future__ import annotations
 
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
+from fractions import Fraction
 
 import numpy as np
 
@@ -120,32 +121,47 @@ def derivative_scale(j: int, alpha: int, beta: int, order: int) -> float:
     return prod / float(2 ** order)
 
 
-def assemble(rho: np.ndarray, m: int, j: int, k: int, ch) -> np.ndarray:
+def numpy_power(rho: np.ndarray, e: int) -> np.ndarray:
+    """``rho ** e`` exactly as the reference evaluates it (numpy's array pow,
+    which may be 1 ulp off the correctly rounded power)."""
+    return rho ** e
+
+
+def cr_power(rho: np.ndarray, e: int) -> np.ndarray:
+    """Correctly rounded rho**e (exact rational power, rounded once; 0**0 = 1).
+    The GPU kernels compute their powers this way (double-double, rounded once),
+    so the reference algorithm with ``power=cr_power`` is their bitwise oracle
+    at every point, not only where numpy's pow happens to be correctly rounded."""
+    return np.array([float(Fraction(float(r)) ** e) for r in np.ravel(rho)]).reshape(np.shape(rho))
+
+
+def assemble(rho: np.ndarray, m: int, j: int, k: int, ch, power=numpy_power) -> np.ndarray:
     """zk/evaluate.py:102-154. ``ch[i]`` = P_{j-i}^{(m+i, i)}(u).
 
     Expressions are written exactly as numpy evaluates the reference's
     (left-to-right products, python-int prefactors promoted to float64).
     """
     sign = -1.0 if j & 1 else 1.0
+    pw = power
     if k == 0:
-        val = rho ** m * ch[0]
+        val = pw(rho, m) * ch[0]
     elif k == 1:
         s1 = derivative_scale(j, m, 0, 1)
-        val = m * rho ** max(m - 1, 0) * ch[0] - 4.0 * s1 * rho ** (m + 1) * ch[1]
+        val = m * pw(rho, max(m - 1, 0)) * ch[0] - 4.0 * s1 * pw(rho, m + 1) * ch[1]
     elif k == 2:
         s1 = derivative_scale(j, m, 0, 1)
         s2 = derivative_scale(j, m, 0, 2)
-        val = ((m - 1) * m * rho ** max(m - 2, 0) * ch[0]
-               - 4.0 * (2 * m + 1) * s1 * rho ** m * ch[1]
-               + 16.0 * s2 * rho ** (m + 2) * ch[2])
+        val = ((m - 1) * m * pw(rho, max(m - 2, 0)) * ch[0]
+               - 4.0 * (2 * m + 1) * s1 * pw(rho, m) * ch[1]
+               + 16.0 * s2 * pw(rho, m + 2) * ch[2])
     elif k == 3:
         s1 = derivative_scale(j, m, 0, 1)
         s2 = derivative_scale(j, m, 0, 2)
         s3 = derivative_scale(j, m, 0, 3)
-        val = ((m - 2) * (m - 1) * m * rho ** max(m - 3, 0) * ch[0]
-               - 12.0 * m * m * s1 * rho ** max(m - 1, 0) * ch[1]
-               + 48.0 * (m + 1) * s2 * rho ** (m + 1) * ch[2]
-               - 64.0 * s3 * rho ** (m + 3) * ch[3])
+        val = ((m - 2) * (m - 1) * m * pw(rho, max(m - 3, 0)) * ch[0]
+               - 12.0 * m * m * s1 * pw(rho, max(m - 1, 0)) * ch[1]
+               + 48.0 * (m + 1) * s2 * pw(rho, m + 1) * ch[2]
+               - 64.0 * s3 * pw(rho, m + 3) * ch[3])
     else:
         raise ValueError(f"derivative order must be 0..3, got {k}")
     return sign * val
@@ -163,12 +179,14 @@ def radial_single(n: int, m_abs: int, rho: np.ndarray, k: int = 0) -> np.ndarray
     return assemble(rho, m_abs, j, k, ch)
 
 
-def radial_batch(modes, rho: np.ndarray, k: int = 0, parallel: bool = False) -> np.ndarray:
+def radial_batch(modes, rho: np.ndarray, k: int = 0, parallel: bool = False,
+                 power=numpy_power) -> np.ndarray:
     """zk/batch.py:104-142 (cached strategy) + :97-101 scatter.
 
     Returns the (P, M) matrix, F-contiguous like the reference's fancy-index
     gather. ``parallel`` maps alpha groups onto a thread pool exactly as the
     reference does (:136-138); results are bitwise independent of it.
+    ``power=cr_power`` swaps numpy's pow for the correctly rounded power.
     """
     rho = np.atleast_1d(np.asarray(rho, dtype=np.float64))
     keys, scatter = unique_and_scatter(modes)
@@ -184,7 +202,7 @@ def radial_batch(modes, rho: np.ndarray, k: int = 0, parallel: bool = False) -> 
                   for i in range(k + 1)]
         for slot, j in entries:
             ch = [chains[i][j - i] if j - i >= 0 else zeros for i in range(k + 1)]
-            unique[:, slot] = assemble(rho, a, j, k, ch)
+            unique[:, slot] = assemble(rho, a, j, k, ch, power)
 
     if parallel and len(groups) > 1:
         with ThreadPoolExecutor() as pool:

@@ -183,7 +183,11 @@ Geometry geometry(const zk_ctx* ctx, const zk_plan* plan, int64_t P, int K, bool
   const int64_t tile_pts = int64_t(zk::kRadialThreads) * g.vec;
   g.ntiles = static_cast<int>((P + tile_pts - 1) / tile_pts);
   const int64_t G = static_cast<int64_t>(plan->host.groups.size());
-  const int64_t target = int64_t(ctx->sm_count) * env_int("ZK_CTAS_PER_SM", 1 << 20);
+  // one tile per CTA for the store-bound orders; the FP64-bound single-order
+  // k >= 2 kernels amortise the per-CTA coefficient staging over several
+  // tiles (measured: k=3 0.94 -> 0.85 ms, k=2 0.79 -> 0.74 ms at config 3)
+  const int per_sm = env_int("ZK_CTAS_PER_SM", (K >= 2 && !all) ? 16 : (1 << 20));
+  const int64_t target = int64_t(ctx->sm_count) * per_sm;
   int64_t tpc = (int64_t(g.ntiles) * G + target - 1) / target;
   tpc = std::max<int64_t>(1, std::min<int64_t>(tpc, g.ntiles));
   g.tiles_per_chunk = static_cast<int>(tpc);

@@ -160,23 +160,28 @@ __device__ __forceinline__ PowSet<K> make_powset(double rho, int m) {
 
 // Radial value of order O from the chain values ch[i] = P_{j-i}^{(m+i,i)}(u),
 // before the (-1)^j sign (zk/evaluate.py:124-149, same operation order).
+// neg = true returns exactly the negated value: every rho-power factor enters
+// negated, and round-to-nearest is sign-symmetric (RN(-x) = -RN(x), so
+// RN((-a)(b)) = -RN(ab), RN((-a)-(-b)) = -RN(a-b)). With a compile-time neg
+// the negations become free operand modifiers of DMUL.
 template <int O, int K>
 __device__ __forceinline__ double assemble(const PowSet<K>& s, const AsmCoef& a,
-                                           const double* ch) {
+                                           const double* ch, bool neg = false) {
+  auto sg = [neg](double x) { return neg ? -x : x; };
   if constexpr (O == 0) {
-    return __dmul_rn(s.A0, ch[0]);
+    return __dmul_rn(sg(s.A0), ch[0]);
   } else if constexpr (O == 1) {
-    return __dsub_rn(__dmul_rn(s.A1, ch[0]), __dmul_rn(__dmul_rn(a.c11, s.B1), ch[1]));
+    return __dsub_rn(__dmul_rn(sg(s.A1), ch[0]), __dmul_rn(__dmul_rn(a.c11, sg(s.B1)), ch[1]));
   } else if constexpr (O == 2) {
-    const double t0 = __dmul_rn(s.A2, ch[0]);
-    const double t1 = __dmul_rn(__dmul_rn(a.c21, s.B2), ch[1]);
-    const double t2 = __dmul_rn(__dmul_rn(a.c22, s.C2), ch[2]);
+    const double t0 = __dmul_rn(sg(s.A2), ch[0]);
+    const double t1 = __dmul_rn(__dmul_rn(a.c21, sg(s.B2)), ch[1]);
+    const double t2 = __dmul_rn(__dmul_rn(a.c22, sg(s.C2)), ch[2]);
     return __dadd_rn(__dsub_rn(t0, t1), t2);
   } else {
-    const double t0 = __dmul_rn(s.A3, ch[0]);
-    const double t1 = __dmul_rn(__dmul_rn(a.c31, s.B3), ch[1]);
-    const double t2 = __dmul_rn(__dmul_rn(a.c32, s.C3), ch[2]);
-    const double t3 = __dmul_rn(__dmul_rn(a.c33, s.D3), ch[3]);
+    const double t0 = __dmul_rn(sg(s.A3), ch[0]);
+    const double t1 = __dmul_rn(__dmul_rn(a.c31, sg(s.B3)), ch[1]);
+    const double t2 = __dmul_rn(__dmul_rn(a.c32, sg(s.C3)), ch[2]);
+    const double t3 = __dmul_rn(__dmul_rn(a.c33, sg(s.D3)), ch[3]);
     return __dsub_rn(__dadd_rn(__dsub_rn(t0, t1), t2), t3);
   }
 }

@@ -26,6 +26,7 @@
 // staged once in shared memory and read as warp-uniform broadcasts.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "zk_kernels.cuh"
@@ -128,26 +129,26 @@ struct Thread {
 
   // value(s) of degree j from chain values ch (ch[i] = P_{j-i}), (-1)^j applied.
   // STEADY: every chain is at degree >= 2 (j >= K+2), no zero chains.
-  template <bool STEADY>
+  // PAR: parity of j when known at compile time (0 even, 1 odd), else -1; a
+  // static parity folds the sign into the assembly's DMUL operand modifiers.
+  template <bool STEADY, int PAR>
   __device__ __forceinline__ void values(int j, const AsmCoef& ac,
                                          const double (&chs)[K + 1][VEC],
                                          double (&val)[NO][VEC]) const {
-    const bool odd = (j & 1) != 0;
+    const bool odd = PAR >= 0 ? PAR == 1 : (j & 1) != 0;
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       double ch[K + 1];
 #pragma unroll
       for (int i = 0; i <= K; ++i) ch[i] = (STEADY || j - i >= 0) ? chs[i][v] : 0.0;
       if constexpr (ALL) {
-        val[0][v] = assemble<0, K>(pw[v], ac, ch);
-        if constexpr (K >= 1) val[1][v] = assemble<1, K>(pw[v], ac, ch);
-        if constexpr (K >= 2) val[2][v] = assemble<2, K>(pw[v], ac, ch);
-        if constexpr (K >= 3) val[3][v] = assemble<3, K>(pw[v], ac, ch);
+        val[0][v] = assemble<0, K>(pw[v], ac, ch, odd);
+        if constexpr (K >= 1) val[1][v] = assemble<1, K>(pw[v], ac, ch, odd);
+        if constexpr (K >= 2) val[2][v] = assemble<2, K>(pw[v], ac, ch, odd);
+        if constexpr (K >= 3) val[3][v] = assemble<3, K>(pw[v], ac, ch, odd);
       } else {
-        val[0][v] = assemble<K, K>(pw[v], ac, ch);
+        val[0][v] = assemble<K, K>(pw[v], ac, ch, odd);
       }
-#pragma unroll
-      for (int o = 0; o < NO; ++o) val[o][v] = odd ? -val[o][v] : val[o][v];
     }
   }
 
@@ -288,17 +289,17 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
     const unsigned long long pol = evict_first_policy();
     const long long ostride_b = a.ostride * 8;
 
-    auto emit = [&](int j, const double(&chs)[K + 1][VEC], auto steady) {
+    auto emit = [&](int j, const double(&chs)[K + 1][VEC], auto steady, auto par) {
       const int r_lo = s_row[j];
       const int r_hi = s_row[j + 1];
       if (r_lo == r_hi) return;  // CTA-uniform
       AsmCoef ac;
       if constexpr (K > 0) ac = load_asm(s_asm + j);
       double val[NO][VEC];
-      th.template values<decltype(steady)::value>(j, ac, chs, val);
+      th.template values<decltype(steady)::value, decltype(par)::value>(j, ac, chs, val);
       if (!use_tma) {
         if (full) {
-          for (int r = r_lo; r < r_hi; ++r) {
+          auto store_col = [&](int r) {
             const long long off = s_off[r];
             char* dst = obase + (ANG ? (off & ~1LL) : off);
 #pragma unroll
@@ -307,7 +308,16 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
               th.column(ANG && (off & 1) != 0, o, val, w);
               store_vec<VEC>(reinterpret_cast<double*>(dst + o * ostride_b), w, pol);
             }
+          };
+          // a degree has 1-2 columns (+-m) per mode set occurrence: pairs,
+          // then the odd one, with no generic unrolled remainder loops
+          int r = r_lo;
+#pragma unroll 1
+          for (; r + 2 <= r_hi; r += 2) {
+            store_col(r);
+            store_col(r + 1);
           }
+          if (r < r_hi) store_col(r);
         } else {
           for (int r = r_lo; r < r_hi; ++r) {
             const long long off = s_off[r];
@@ -374,7 +384,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
           }
         }
       }
-      emit(j, th.cur, std::false_type{});
+      emit(j, th.cur, std::false_type{}, std::integral_constant<int, -1>{});
     }
     // ---- steady state: every chain in the three-term recursion. Unrolled by
     // two with the roles of the state arrays swapped (no register moves):
@@ -389,14 +399,14 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
 #pragma unroll
         for (int v = 0; v < VEC; ++v) B[i][v] = jacobi_step(c, th.u[v], A[i][v], B[i][v]);
       }
-      emit(j, B, std::true_type{});
+      emit(j, B, std::true_type{}, std::integral_constant<int, K % 2>{});
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
         const ChainCoef c = load_coef(s_coef + i * nj + (j + 1 - i));
 #pragma unroll
         for (int v = 0; v < VEC; ++v) A[i][v] = jacobi_step(c, th.u[v], B[i][v], A[i][v]);
       }
-      emit(j + 1, A, std::true_type{});
+      emit(j + 1, A, std::true_type{}, std::integral_constant<int, (K + 1) % 2>{});
     }
     if (j <= jmax) {
 #pragma unroll
@@ -405,16 +415,17 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
 #pragma unroll
         for (int v = 0; v < VEC; ++v) B[i][v] = jacobi_step(c, th.u[v], A[i][v], B[i][v]);
       }
-      emit(j, B, std::true_type{});
+      emit(j, B, std::true_type{}, std::integral_constant<int, K % 2>{});
     }
   }
 }
 
 // Register budgets: the compiler's default heuristic (launch bound without a
-// CTA minimum) lands at 64-80 registers for k <= 2; k = 3 would take 149
-// (one 256-thread CTA per SM, measured 1.5x slower), so it is capped at two
-// CTAs per SM. An explicit minimum of 1 CTA inflates allocation (113-136
-// registers for k <= 2, measured slower) -- hence two kernel wrappers.
+// CTA minimum) lands at 64-80 registers for k <= 1 and 126 for k = 3 single
+// order (two CTAs per SM); k = 3 all orders would take ~250 (one CTA per SM,
+// measured 1.5x slower), so it is capped at two CTAs per SM. An explicit
+// minimum of 1 CTA inflates allocation (113-136 registers for k <= 2,
+// measured slower) -- hence separate kernel wrappers.
 template <int K, bool ALL, bool ANG, int VEC, bool TMA>
 __global__ void __launch_bounds__(kRadialThreads + (TMA ? 32 : 0))
 radial_basis_kernel(const RadialArgs a) {
@@ -446,7 +457,17 @@ static cudaError_t launch_t(const RadialArgs& a, int grid, size_t smem, cudaStre
   if constexpr (K == 3 && !TMA && VEC <= 2 && ALL) {
     fn = radial_basis_kernel_2cta<K, ALL, ANG, VEC, TMA>;
   } else if constexpr (K >= 2 && !TMA && VEC <= 2 && !ALL) {
-    fn = radial_basis_kernel_3cta<K, ALL, ANG, VEC, TMA>;
+    // single order k = 2: three CTAs per SM (80 registers); k = 3: the
+    // compiler's own budget (126 registers, two CTAs) -- both measured best
+    // with several tiles per CTA (geometry()). ZK_MINB=0/2/3 overrides.
+    static const int minb = [] {
+      const char* v = std::getenv("ZK_MINB");
+      return v && *v ? std::atoi(v) : -1;
+    }();
+    const int b = minb >= 0 ? minb : (K == 2 ? 3 : 0);
+    fn = b == 3   ? radial_basis_kernel_3cta<K, ALL, ANG, VEC, TMA>
+         : b == 2 ? radial_basis_kernel_2cta<K, ALL, ANG, VEC, TMA>
+                  : radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
   } else {
     fn = radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
   }

@@ -2,7 +2,8 @@
 reference's own property tests (tests/test_evaluate.py:224-251,
 tests/test_batch.py:170-192): arbitrary mode requests and arbitrary binary64
 points against the binary128 oracle (== the exact oracle) and the reference
-algorithm."""
+algorithm. Examples are derandomized (stable across runs); tools/prop_hunt.py
+explores fresh random requests against the same bitwise claim."""
 
 import numpy as np
 import pytest
@@ -19,23 +20,31 @@ points = st.lists(st.floats(0.0, 1.0, allow_nan=False), min_size=1, max_size=40)
 
 
 @given(st.lists(mode, min_size=1, max_size=30), points, st.integers(0, 3))
-@settings(max_examples=60, deadline=None)
+@settings(max_examples=60, deadline=None, derandomize=True)
 def test_batch_matches_exact_oracle_at_arbitrary_points(modes, pts, k):
     grid = np.array(pts)
     t, _ = zb.evaluate_batch(zb.BatchRequest(modes=zb.as_mode_set(modes), grid=grid,
                                              deriv_order=k))
     exact = orc.quad_table(modes, grid, k)
-    ref = orc.radial_batch(modes, grid, k)
     scale = np.maximum(1.0, np.abs(exact).max(axis=0))
     err = np.abs(t.values - exact).max(axis=0) / scale
     assert (err <= 1e-12).all()
-    # and on par with the reference algorithm's own error
-    err_ref = np.abs(ref - exact).max(axis=0) / scale
-    assert (err <= 2 * err_ref + 2e-16).all()
+    # bitwise the reference algorithm (zk/batch.py + zk/evaluate.py) once its
+    # numpy pow is replaced by the correctly rounded power the kernels use:
+    # numpy's SIMD pow is up to 1 ulp off, which the derivative assembly's
+    # cancellation amplifies to a few ulps either way (tools/prop_hunt.py)
+    # (below ~1e-250 the double-double power loses its low word to underflow,
+    # so only the absolute size is checked there)
+    ref_cr = orc.radial_batch(modes, grid, k, power=orc.cr_power)
+    tiny = np.abs(ref_cr) < 1e-250
+    bad = np.argwhere(~tiny & (t.values != ref_cr))
+    assert bad.size == 0, [(modes[c], repr(grid[p]), k, repr(t.values[p, c]), repr(ref_cr[p, c]))
+                           for p, c in bad[:4]]
+    assert (np.abs(t.values - ref_cr)[tiny] <= 1e-250).all()
 
 
 @given(st.lists(mode, min_size=1, max_size=12), points, st.integers(0, 2))
-@settings(max_examples=30, deadline=None)
+@settings(max_examples=30, deadline=None, derandomize=True)
 def test_strategies_and_single_mode_agree_bitwise(modes, pts, k):
     grid = np.array(pts)
     ms = zb.as_mode_set(modes)
@@ -48,7 +57,7 @@ def test_strategies_and_single_mode_agree_bitwise(modes, pts, k):
 
 
 @given(mode, st.floats(0.0, 1.0, allow_nan=False), st.floats(-7.0, 7.0))
-@settings(max_examples=60, deadline=None)
+@settings(max_examples=60, deadline=None, derandomize=True)
 def test_zernike_eval_is_radial_times_angular(md, rho, theta):
     n, m = md
     radial = zb.radial_jacobi(n, abs(m), [rho])[0]
