@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import _lib
+from . import _lib, hostpool
 from .modes import Mode, make_mode
 from .tables import angular_grid, radial_grid
 
@@ -99,7 +99,7 @@ def basis_matrix(mode_n: np.ndarray, mode_m: np.ndarray, rho: np.ndarray, k: int
     rho = np.ascontiguousarray(rho, dtype=np.float64)
     P, M = rho.size, int(np.asarray(mode_n).size)
     n_out = k + 1 if (all_orders and k > 0) else 1
-    flat = np.empty(n_out * P * M, dtype=np.float64)
+    flat = hostpool.take(n_out * P * M)
     mats = [flat[o * P * M:(o + 1) * P * M].reshape((P, M), order="F") for o in range(n_out)]
     if theta is not None:
         theta = np.ascontiguousarray(theta, dtype=np.float64)
