@@ -154,8 +154,11 @@ def host_cores():
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    # bound the whole run to ~a minute: fewer points per step when K is large
-    sample = int(min(args.ref_sample, max(500, args.ref_sample * 20 // max(1, args.steps))))
+    # bound the whole run to ~1-2 minutes (~0.3 s per 10^4-point step on 16
+    # cores): the full --ref-sample per step up to 200 steps, fewer points
+    # per step beyond that (small samples understate the CPU rate: numpy's
+    # per-call overhead is amortised over fewer points)
+    sample = int(min(args.ref_sample, max(1000, args.ref_sample * 200 // max(1, args.steps))))
     rate, t, npts, M = cpu_reference_rate(sample, reps=max(1, args.steps),
                                           warmup=max(0, min(args.warmup, 1)))
     cores = host_cores()
@@ -176,17 +179,34 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def max_over_ranks(dist, x: float, local: int) -> float:
+    import torch
+    dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_gpu(args, world, rank, local):
     import torch
 
     import paper_2409_19156_b200 as zb
     from paper_2409_19156_b200 import _lib
 
+    if os.environ.get("ZK_BENCH_BACKEND", "nccl") != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # ZK_BENCH_BACKEND=gloo: functional check of the multi-rank path on one
+        # GPU (NCCL refuses two ranks on one device); numbers from it are not
+        # bench values
+        backend = os.environ.get("ZK_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     modes = zb.full_mode_set(N_RES)
     n_arr, m_arr = zb.modes.mode_arrays(modes)
@@ -237,9 +257,7 @@ def run_gpu(args, world, rank, local):
     t_ms = ev0.elapsed_time(ev1)
     clocks = sampler.stop() if sampler else None
     if dist:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
+        t_ms = max_over_ranks(dist, t_ms, local)
     ms_per_step = t_ms / args.steps
     value = Pg * M / (ms_per_step * 1e-3)  # every rank's points / max-over-ranks time
 
@@ -285,9 +303,7 @@ def run_gpu(args, world, rank, local):
             e2e_step()
         te = (time.perf_counter() - t0) / e2e_steps
         if dist:
-            tt = torch.tensor([te], dtype=torch.float64, device=f"cuda:{local}")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt.item())
+            te = max_over_ranks(dist, te, local)
         host_view = np.ctypeslib.as_array(ctypes.cast(hbuf.value, ctypes.POINTER(ctypes.c_double)),
                                           shape=(P * M,))
         e2e_ok = bool(np.array_equal(host_view[:P], out[0].cpu().numpy()))
