@@ -305,14 +305,20 @@ def run_gpu(args, world, rank, local):
         if dist:
             te = max_over_ranks(dist, te, local)
         host_view = np.ctypeslib.as_array(ctypes.cast(hbuf.value, ctypes.POINTER(ctypes.c_double)),
-                                          shape=(P * M,))
-        e2e_ok = bool(np.array_equal(host_view[:P], out[0].cpu().numpy()))
+                                          shape=(M, P))
+        e2e_ok = bool(np.array_equal(host_view, out.cpu().numpy()))  # every column
+        del host_view
         _lib.lib.zk_host_free(hbuf)
         _lib.lib.zk_host_free(rbuf)
+        U = plan.info()["U"]
         e2e = {"value": Pg * M / te, "unit": UNIT, "h2d_bytes_per_step": 8 * P,
-               "d2h_bytes_per_step": 8 * P * M, "ms_per_step": te * 1e3,
-               "path": "zk_radial_eval(ZK_HOST_INPUT|ZK_HOST_OUTPUT), pinned host buffers, "
-                       "chunked 2-stream D2H pipeline", "matches_device": e2e_ok}
+               "d2h_bytes_per_step": 8 * P * U, "host_filled_bytes_per_step": 8 * P * (M - U),
+               "ms_per_step": te * 1e3,
+               "path": "zk_radial_eval(ZK_HOST_INPUT|ZK_HOST_OUTPUT) into pinned host buffers: "
+                       "chunked 2-stream pipeline, the U unique (n,|m|) columns cross PCIe, "
+                       "the M-U repeated (+-m) columns are host copies of them (the "
+                       "reference's unique->scatter, zk/batch.py:97-101)",
+               "matches_device": e2e_ok}
 
     if rank != 0:
         if dist:

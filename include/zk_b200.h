@@ -35,7 +35,12 @@
  *     Mode invariant (zk/modes.py:37-43). Invalid modes -> ZK_EINVAL.
  *   - Memory: pointers are device pointers unless the ZK_HOST_* flag for
  *     that argument is set. Host outputs are written through a chunked,
- *     double-buffered device->host pipeline. Caller owns every buffer.
+ *     double-buffered device->host pipeline; for the radial basis only the
+ *     unique (n, |m|) columns cross PCIe and repeated columns (+-m pairs,
+ *     duplicates) are filled on the host from their key's first column
+ *     (the reference's unique -> scatter, zk/batch.py:97-101). Pinned host
+ *     buffers (zk_host_alloc) get direct DMA; pageable ones go through
+ *     pinned bounce buffers. Caller owns every buffer.
  *   - Reentrant: state lives in zk_ctx (one CUDA stream + scratch per ctx).
  *     Distinct contexts may be used from distinct threads concurrently.
  *   - There is no CPU fallback: without a usable CUDA device every compute

@@ -129,6 +129,7 @@ struct zk_ctx {
   size_t hbounce_bytes[2] = {0, 0};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   HostPool* pool = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;  // per-chunk D2H completion (unique-column path)
   int64_t launches = 0;
   std::mutex mu;  // one call at a time per ctx
 };
@@ -143,6 +144,19 @@ struct zk_plan {
   const int32_t* cols = nullptr;
   const zk::ChainCoef* coef = nullptr;
   const zk::AsmCoef* asmc = nullptr;
+  // Unique-column view for host outputs of the radial basis (built on first
+  // use): the kernel writes one column per unique (n, |m|) key -- in the order
+  // of each key's first column -- and only those cross PCIe; every other
+  // column is a host copy of its key's first column. This is the reference's
+  // own unique -> scatter structure (zk/batch.py:97-101, zk/modes.py:108-125).
+  struct Run {
+    int64_t u0, c0, len;  // unique columns u0.. land in output columns c0..
+  };
+  zk_plan* uplan = nullptr;
+  std::vector<int64_t> u_first;                  // key -> its first output column
+  std::vector<Run> runs;                         // contiguous first-column runs
+  std::vector<std::pair<int64_t, int64_t>> dup;  // (output column, key) of the others
+  bool uview = false;
 };
 
 namespace {
@@ -163,6 +177,48 @@ int ensure_scratch(zk_ctx* ctx, int slot, size_t bytes) {
     return fail(ZK_ENOMEM, std::string("scratch allocation failed: ") + cudaGetErrorString(e));
   }
   ctx->scratch_bytes[slot] = bytes;
+  return ZK_OK;
+}
+
+// Build the plan's unique-column view (see zk_plan); ZK_OK or an error.
+int ensure_unique_view(zk_plan* plan) {
+  if (plan->uview) return ZK_OK;
+  const zk::HostPlan& h = plan->host;
+  const int64_t U = static_cast<int64_t>(h.key_n.size());
+  plan->u_first.assign(U, -1);
+  plan->dup.clear();
+  for (int64_t c = 0; c < h.M; ++c) {
+    const int64_t u = h.scatter[c];
+    if (plan->u_first[u] < 0)
+      plan->u_first[u] = c;
+    else
+      plan->dup.emplace_back(c, u);
+  }
+  plan->runs.clear();
+  for (int64_t u = 0; u < U; ++u) {
+    if (!plan->runs.empty()) {
+      zk_plan::Run& r = plan->runs.back();
+      if (r.u0 + r.len == u && r.c0 + r.len == plan->u_first[u]) {
+        ++r.len;
+        continue;
+      }
+    }
+    plan->runs.push_back({u, plan->u_first[u], 1});
+  }
+  std::vector<int32_t> kn(h.key_n), km(U);
+  for (int64_t u = 0; u < U; ++u) km[u] = std::abs(h.key_m[u]);
+  int rc = zk_plan_create(plan->ctx, kn.data(), km.data(), U, h.max_order, &plan->uplan);
+  if (rc) return rc;
+  plan->uview = true;
+  return ZK_OK;
+}
+
+int ensure_chunk_events(zk_ctx* ctx, size_t n) {
+  while (ctx->chunk_ev.size() < n) {
+    cudaEvent_t e;
+    ZK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
+    ctx->chunk_ev.push_back(e);
+  }
   return ZK_OK;
 }
 
@@ -312,8 +368,20 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
 
   // host output: chunk the points, double-buffered compute -> D2H pipeline on
   // two streams so chunk c's copy overlaps chunk c+1's kernel.
+  // Radial basis with repeated keys (every +-m pair of a full set): the chunk
+  // holds the unique-key columns only; PCIe carries U instead of M columns and
+  // the host fills the other columns from their key's first column.
+  zk_plan* mplan = const_cast<zk_plan*>(plan);
+  const bool uniq = !ang && static_cast<int64_t>(plan->host.key_n.size()) < M &&
+                    env_int("ZK_UNIQUE_D2H", 1) != 0;
+  if (uniq) {
+    int rc = ensure_unique_view(mplan);
+    if (rc) return rc;
+  }
+  const zk_plan* kplan = uniq ? plan->uplan : plan;  // what the kernel evaluates
+  const int64_t Mk = kplan->host.M;                   // columns per chunk
   const size_t budget = size_t(256) << 20;  // bytes of basis per slot
-  const size_t per_point = size_t(8) * size_t(M) * NO;
+  const size_t per_point = size_t(8) * size_t(Mk) * NO;
   int64_t pc = static_cast<int64_t>(budget / per_point);
   pc = std::max<int64_t>(1024, pc / 1024 * 1024);  // whole TMA tiles per chunk
   pc = std::min<int64_t>(pc, (P + 1023) / 1024 * 1024);
@@ -333,6 +401,12 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
                       pa.type == cudaMemoryTypeHost;
   cudaGetLastError();
   const bool bounce = !pinned && env_int("ZK_BOUNCE", 1) != 0;
+  if (bounce || uniq) {
+    if (!ctx->pool) {
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+      ctx->pool = new HostPool(std::min(15u, hw - 1));
+    }
+  }
   if (bounce) {
     for (int s = 0; s < 2; ++s) {
       if (ctx->hbounce_bytes[s] < basis_bytes) {
@@ -349,10 +423,6 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
         ctx->hbounce_bytes[s] = basis_bytes;
       }
     }
-    if (!ctx->pool) {
-      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-      ctx->pool = new HostPool(std::min(15u, hw - 1));
-    }
     // a fresh numpy result is untouched anonymous memory: ask for transparent
     // huge pages so the scatter takes 512x fewer first-touch page faults
     if (env_int("ZK_HUGEPAGE", 1)) {
@@ -364,6 +434,10 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
     }
   }
   const int64_t nchunks = (P + pc - 1) / pc;
+  if (uniq && !bounce) {
+    int rc = ensure_chunk_events(ctx, static_cast<size_t>(nchunks));
+    if (rc) return rc;
+  }
   auto enqueue = [&](int64_t chunk) -> int {
     const int s = static_cast<int>(chunk & 1);
     cudaStream_t st = ctx->pipe[s];
@@ -383,12 +457,20 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
       }
     }
     const int64_t dld = pc;
-    int rc = launch_device(ctx, plan, r_in, t_in, n, k, all, dbasis, dld, dld * M, scalar, st);
+    int rc = launch_device(ctx, kplan, r_in, t_in, n, k, all, dbasis, dld, dld * Mk, scalar, st);
     if (rc) return rc;
     if (bounce) {
-      ZK_CUDA(cudaMemcpyAsync(ctx->hbounce[s], dbasis, size_t(dld) * M * NO * 8,
+      ZK_CUDA(cudaMemcpyAsync(ctx->hbounce[s], dbasis, size_t(dld) * Mk * NO * 8,
                               cudaMemcpyDeviceToHost, st));
       ZK_CUDA(cudaEventRecord(ctx->ev_done[s], st));
+    } else if (uniq) {
+      // each run of unique columns lands in its contiguous output columns
+      for (int o = 0; o < NO; ++o)
+        for (const zk_plan::Run& r : plan->runs)
+          ZK_CUDA(cudaMemcpy2DAsync(out + o * ostride + r.c0 * ld + p0, size_t(ld) * 8,
+                                    dbasis + o * dld * Mk + r.u0 * dld, size_t(dld) * 8,
+                                    size_t(n) * 8, size_t(r.len), cudaMemcpyDeviceToHost, st));
+      ZK_CUDA(cudaEventRecord(ctx->chunk_ev[chunk], st));
     } else {
       for (int o = 0; o < NO; ++o) {
         ZK_CUDA(cudaMemcpy2DAsync(out + o * ostride + p0, size_t(ld) * 8, dbasis + o * dld * M,
@@ -403,11 +485,26 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
       int rc = enqueue(c);
       if (rc) return rc;
     }
+    if (uniq) {  // fill the repeated-key columns of each chunk once it has landed
+      const int64_t nd = static_cast<int64_t>(plan->dup.size());
+      for (int64_t c = 0; c < nchunks; ++c) {
+        ZK_CUDA(cudaEventSynchronize(ctx->chunk_ev[c]));
+        const int64_t p0 = c * pc;
+        const int64_t n = std::min<int64_t>(pc, P - p0);
+        ctx->pool->parallel_for(int64_t(NO) * nd, [&](int64_t i) {
+          const int64_t o = i / nd;
+          const auto& d = plan->dup[i - o * nd];
+          double* base = out + o * ostride + p0;
+          std::memcpy(base + d.first * ld, base + plan->u_first[d.second] * ld, size_t(n) * 8);
+        });
+      }
+    }
   } else {
     for (int64_t c = 0; c < std::min<int64_t>(2, nchunks); ++c) {
       int rc = enqueue(c);
       if (rc) return rc;
     }
+    const int32_t* key_of = plan->host.scatter.data();
     for (int64_t c = 0; c < nchunks; ++c) {
       const int s = static_cast<int>(c & 1);
       ZK_CUDA(cudaEventSynchronize(ctx->ev_done[s]));
@@ -416,7 +513,8 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
       const double* hb = static_cast<const double*>(ctx->hbounce[s]);
       ctx->pool->parallel_for(int64_t(NO) * M, [&](int64_t oc) {
         const int64_t o = oc / M, col = oc - o * M;
-        std::memcpy(out + o * ostride + col * ld + p0, hb + (o * M + col) * pc, size_t(n) * 8);
+        const int64_t src = uniq ? key_of[col] : col;
+        std::memcpy(out + o * ostride + col * ld + p0, hb + (o * Mk + src) * pc, size_t(n) * 8);
       });
       if (c + 2 < nchunks) {
         int rc = enqueue(c + 2);
@@ -505,6 +603,7 @@ int zk_ctx_destroy(zk_ctx* ctx) {
     if (ctx->ev_done[s]) cudaEventDestroy(ctx->ev_done[s]);
     if (ctx->hbounce[s]) cudaFreeHost(ctx->hbounce[s]);
   }
+  for (cudaEvent_t e : ctx->chunk_ev) cudaEventDestroy(e);
   delete ctx->pool;
   delete ctx;
   return ZK_OK;
@@ -611,6 +710,7 @@ int zk_plan_create(zk_ctx* ctx, const int32_t* mode_n, const int32_t* mode_m, in
 
 int zk_plan_destroy(zk_plan* plan) {
   if (!plan) return ZK_OK;
+  zk_plan_destroy(plan->uplan);
   if (plan->dmem) {
     cudaSetDevice(plan->ctx->device);
     cudaFree(plan->dmem);

@@ -463,3 +463,49 @@ def test_parallel_shards_over_devices_bitwise(monkeypatch):
                      devices=[0, 0])
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_unique_column_host_output_equals_device_output(pinned):
+    """Host outputs of the radial basis carry only the unique (n, |m|) columns
+    over PCIe and fill the repeated ones on the host (zk_capi.cu, unique view):
+    shuffled, duplicated and sign-flipped modes, several chunks, all orders,
+    ld > P, pinned and pageable destinations -- bitwise the device result."""
+    import ctypes
+
+    rng = np.random.default_rng(21)
+    full = [(md.n, md.m) for md in zb.full_mode_set(60)]
+    pick = [full[i] for i in rng.permutation(len(full))[:900]]
+    pick += pick[:200] + [(n, -m) for n, m in pick[200:400]]
+    modes = zb.as_mode_set(pick)
+    M, P, k = len(modes), 70_001, 2
+    ld = P + 5
+    ostride = ld * M + 3
+    ctx, plan = _plan(modes)
+    grid = rng.uniform(size=P)
+    d_rho = torch.tensor(grid, device="cuda")
+    dev = torch.empty((k + 1) * ostride, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib.zk_radial_eval(ctx.handle, plan.handle, d_rho.data_ptr(), P, k, 1,
+                                       dev.data_ptr(), ld, ostride, 0), "radial")
+    ref = dev.cpu().numpy()
+    nbytes = 8 * (k + 1) * ostride
+    if pinned:
+        buf = ctypes.c_void_p()
+        _lib.check(_lib.lib.zk_host_alloc(nbytes, ctypes.byref(buf)), "zk_host_alloc")
+        host = np.ctypeslib.as_array(ctypes.cast(buf.value, ctypes.POINTER(ctypes.c_double)),
+                                     shape=((k + 1) * ostride,))
+    else:
+        host = np.empty((k + 1) * ostride)
+    host[:] = np.nan
+    _lib.check(_lib.lib.zk_radial_eval(ctx.handle, plan.handle, grid.ctypes.data, P, k, 1,
+                                       host.ctypes.data, ld, ostride,
+                                       _lib.ZK_HOST_INPUT | _lib.ZK_HOST_OUTPUT), "radial")
+    for o in range(k + 1):
+        a = ref[o * ostride:o * ostride + ld * M].reshape(M, ld)[:, :P]
+        b = host[o * ostride:o * ostride + ld * M].reshape(M, ld)
+        assert np.array_equal(a, b[:, :P]), o
+        assert np.isnan(b[:, P:]).all()  # row padding untouched
+    if pinned:
+        del host
+        _lib.lib.zk_host_free(buf)
