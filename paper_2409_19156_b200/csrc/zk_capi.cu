@@ -145,19 +145,25 @@ struct zk_plan {
   const int32_t* cols = nullptr;
   const zk::ChainCoef* coef = nullptr;
   const zk::AsmCoef* asmc = nullptr;
-  // Unique-column view for host outputs of the radial basis (built on first
-  // use): the kernel writes one column per unique (n, |m|) key -- in the order
-  // of each key's first column -- and only those cross PCIe; every other
-  // column is a host copy of its key's first column. This is the reference's
-  // own unique -> scatter structure (zk/batch.py:97-101, zk/modes.py:108-125).
+  // Unique-column views for host outputs of the radial basis (built on first
+  // use): the kernel writes the "sent" columns -- one per unique (n, |m|)
+  // key, its first column, plus optionally a share of the repeated columns --
+  // and only those cross PCIe; every other column is a host copy of its key's
+  // first column. This is the reference's own unique -> scatter structure
+  // (zk/batch.py:97-101, zk/modes.py:108-125). (Sending a share of the
+  // repeated columns over PCIe as well, to offload the host fill, measured
+  // slower at every share: 5-30 % -> +1..+9 ms at config 2.)
   struct Run {
-    int64_t u0, c0, len;  // unique columns u0.. land in output columns c0..
+    int64_t s0, c0, len;  // sent columns s0.. land in output columns c0..
   };
-  zk_plan* uplan = nullptr;
-  std::vector<int64_t> u_first;                  // key -> its first output column
-  std::vector<Run> runs;                         // contiguous first-column runs
-  std::vector<std::pair<int64_t, int64_t>> dup;  // (output column, key) of the others
-  bool uview = false;
+  struct UView {
+    zk_plan* kplan = nullptr;                        // plan over the sent columns
+    std::vector<int64_t> slot;                       // output column -> sent slot to copy
+    std::vector<Run> runs;                           // contiguous sent-column runs
+    std::vector<std::pair<int64_t, int64_t>> fill;   // (output column, source column)
+    bool built = false;
+  };
+  UView uv;
 };
 
 namespace {
@@ -183,34 +189,51 @@ int ensure_scratch(zk_ctx* ctx, int slot, size_t bytes) {
 
 // Build the plan's unique-column view (see zk_plan); ZK_OK or an error.
 int ensure_unique_view(zk_plan* plan) {
-  if (plan->uview) return ZK_OK;
+  zk_plan::UView& v = plan->uv;
+  if (v.built) return ZK_OK;
   const zk::HostPlan& h = plan->host;
+  const int64_t M = h.M;
   const int64_t U = static_cast<int64_t>(h.key_n.size());
-  plan->u_first.assign(U, -1);
-  plan->dup.clear();
-  for (int64_t c = 0; c < h.M; ++c) {
+  std::vector<int64_t> first(U, -1);
+  std::vector<char> sent(M, 0);
+  for (int64_t c = 0; c < M; ++c) {
     const int64_t u = h.scatter[c];
-    if (plan->u_first[u] < 0)
-      plan->u_first[u] = c;
-    else
-      plan->dup.emplace_back(c, u);
+    if (first[u] < 0) {
+      first[u] = c;
+      sent[c] = 1;
+    }
   }
-  plan->runs.clear();
-  for (int64_t u = 0; u < U; ++u) {
-    if (!plan->runs.empty()) {
-      zk_plan::Run& r = plan->runs.back();
-      if (r.u0 + r.len == u && r.c0 + r.len == plan->u_first[u]) {
+  std::vector<int32_t> kn, km;
+  std::vector<int64_t> slot_of(M, -1);
+  for (int64_t c = 0; c < M; ++c)
+    if (sent[c]) {
+      slot_of[c] = static_cast<int64_t>(kn.size());
+      kn.push_back(h.key_n[h.scatter[c]]);
+      km.push_back(std::abs(h.key_m[h.scatter[c]]));
+    }
+  v.slot.assign(M, 0);
+  v.fill.clear();
+  v.runs.clear();
+  for (int64_t c = 0; c < M; ++c) {
+    const int64_t src = sent[c] ? c : first[h.scatter[c]];
+    v.slot[c] = slot_of[src];
+    if (!sent[c]) {
+      v.fill.emplace_back(c, src);
+      continue;
+    }
+    if (!v.runs.empty()) {
+      zk_plan::Run& r = v.runs.back();
+      if (r.s0 + r.len == slot_of[c] && r.c0 + r.len == c) {
         ++r.len;
         continue;
       }
     }
-    plan->runs.push_back({u, plan->u_first[u], 1});
+    v.runs.push_back({slot_of[c], c, 1});
   }
-  std::vector<int32_t> kn(h.key_n), km(U);
-  for (int64_t u = 0; u < U; ++u) km[u] = std::abs(h.key_m[u]);
-  int rc = zk_plan_create(plan->ctx, kn.data(), km.data(), U, h.max_order, &plan->uplan);
+  int rc = zk_plan_create(plan->ctx, kn.data(), km.data(), static_cast<int64_t>(kn.size()),
+                          h.max_order, &v.kplan);
   if (rc) return rc;
-  plan->uview = true;
+  v.built = true;
   return ZK_OK;
 }
 
@@ -401,17 +424,26 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
   // host output: chunk the points, double-buffered compute -> D2H pipeline on
   // two streams so chunk c's copy overlaps chunk c+1's kernel.
   // Radial basis with repeated keys (every +-m pair of a full set): the chunk
-  // holds the unique-key columns only; PCIe carries U instead of M columns and
-  // the host fills the other columns from their key's first column.
+  // holds the sent columns only (zk_plan::UView); PCIe carries ~U instead of M
+  // columns and the host fills the others from their key's first column.
+  // Pageable destination (e.g. a fresh numpy array): D2H into pinned bounce
+  // buffers, then the host pool scatters each chunk into place in parallel.
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  const bool bounce = !pinned && env_int("ZK_BOUNCE", 1) != 0;
   zk_plan* mplan = const_cast<zk_plan*>(plan);
   const bool uniq = !ang && static_cast<int64_t>(plan->host.key_n.size()) < M &&
                     env_int("ZK_UNIQUE_D2H", 1) != 0;
+  const zk_plan::UView* uv = nullptr;
   if (uniq) {
     int rc = ensure_unique_view(mplan);
     if (rc) return rc;
+    uv = &plan->uv;
   }
-  const zk_plan* kplan = uniq ? plan->uplan : plan;  // what the kernel evaluates
-  const int64_t Mk = kplan->host.M;                   // columns per chunk
+  const zk_plan* kplan = uniq ? uv->kplan : plan;  // what the kernel evaluates
+  const int64_t Mk = kplan->host.M;                 // columns per chunk
   const size_t budget = size_t(env_int("ZK_CHUNK_MB", 256)) << 20;  // basis bytes per slot
   const size_t per_point = size_t(8) * size_t(Mk) * NO;
   int64_t pc = static_cast<int64_t>(budget / per_point);
@@ -426,17 +458,10 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
   // the pipeline must start after work already queued on the launch stream
   ZK_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
   for (int s = 0; s < 2; ++s) ZK_CUDA(cudaStreamWaitEvent(ctx->pipe[s], ctx->ev_start, 0));
-  // pageable destination (e.g. a fresh numpy array): D2H into pinned bounce
-  // buffers, then the host pool scatters each chunk into place in parallel
-  cudaPointerAttributes pa{};
-  const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess &&
-                      pa.type == cudaMemoryTypeHost;
-  cudaGetLastError();
-  const bool bounce = !pinned && env_int("ZK_BOUNCE", 1) != 0;
   if (bounce || uniq) {
     if (!ctx->pool) {
       const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-      ctx->pool = new HostPool(std::min(15u, hw - 1));
+      ctx->pool = new HostPool(static_cast<unsigned>(std::max(0, env_int("ZK_HOST_THREADS", static_cast<int>(std::min(16u, hw))) - 1)));
     }
   }
   if (bounce) {
@@ -496,11 +521,11 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
                               cudaMemcpyDeviceToHost, st));
       ZK_CUDA(cudaEventRecord(ctx->ev_done[s], st));
     } else if (uniq) {
-      // each run of unique columns lands in its contiguous output columns
+      // each run of sent columns lands in its contiguous output columns
       for (int o = 0; o < NO; ++o)
-        for (const zk_plan::Run& r : plan->runs)
+        for (const zk_plan::Run& r : uv->runs)
           ZK_CUDA(cudaMemcpy2DAsync(out + o * ostride + r.c0 * ld + p0, size_t(ld) * 8,
-                                    dbasis + o * dld * Mk + r.u0 * dld, size_t(dld) * 8,
+                                    dbasis + o * dld * Mk + r.s0 * dld, size_t(dld) * 8,
                                     size_t(n) * 8, size_t(r.len), cudaMemcpyDeviceToHost, st));
       ZK_CUDA(cudaEventRecord(ctx->chunk_ev[chunk], st));
     } else {
@@ -518,16 +543,16 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
       if (rc) return rc;
     }
     if (uniq) {  // fill the repeated-key columns of each chunk once it has landed
-      const int64_t nd = static_cast<int64_t>(plan->dup.size());
+      const int64_t nd = static_cast<int64_t>(uv->fill.size());
       for (int64_t c = 0; c < nchunks; ++c) {
         ZK_CUDA(cudaEventSynchronize(ctx->chunk_ev[c]));
         const int64_t p0 = c * pc;
         const int64_t n = std::min<int64_t>(pc, P - p0);
         ctx->pool->parallel_for(int64_t(NO) * nd, [&](int64_t i) {
           const int64_t o = i / nd;
-          const auto& d = plan->dup[i - o * nd];
+          const auto& d = uv->fill[i - o * nd];
           double* base = out + o * ostride + p0;
-          column_copy(base + d.first * ld, base + plan->u_first[d.second] * ld, size_t(n));
+          column_copy(base + d.first * ld, base + d.second * ld, size_t(n));
         });
       }
     }
@@ -536,7 +561,6 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
       int rc = enqueue(c);
       if (rc) return rc;
     }
-    const int32_t* key_of = plan->host.scatter.data();
     for (int64_t c = 0; c < nchunks; ++c) {
       const int s = static_cast<int>(c & 1);
       ZK_CUDA(cudaEventSynchronize(ctx->ev_done[s]));
@@ -545,7 +569,7 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
       const double* hb = static_cast<const double*>(ctx->hbounce[s]);
       ctx->pool->parallel_for(int64_t(NO) * M, [&](int64_t oc) {
         const int64_t o = oc / M, col = oc - o * M;
-        const int64_t src = uniq ? key_of[col] : col;
+        const int64_t src = uniq ? uv->slot[col] : col;
         column_copy(out + o * ostride + col * ld + p0, hb + (o * Mk + src) * pc, size_t(n));
       });
       if (c + 2 < nchunks) {
@@ -742,7 +766,7 @@ int zk_plan_create(zk_ctx* ctx, const int32_t* mode_n, const int32_t* mode_m, in
 
 int zk_plan_destroy(zk_plan* plan) {
   if (!plan) return ZK_OK;
-  zk_plan_destroy(plan->uplan);
+  zk_plan_destroy(plan->uv.kplan);
   if (plan->dmem) {
     cudaSetDevice(plan->ctx->device);
     cudaFree(plan->dmem);
