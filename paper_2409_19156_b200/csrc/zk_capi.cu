@@ -63,7 +63,6 @@ class HostPool {
     cv_.notify_all();
     for (auto& t : workers_) t.join();
   }
-  unsigned size() const { return static_cast<unsigned>(workers_.size()) + 1; }
   // run fn(i) for i in [0, n) on the pool and the calling thread
   void parallel_for(int64_t n, const std::function<void(int64_t)>& fn) {
     {

@@ -20,6 +20,7 @@ run() {  # name regex skip cmd...
   rm -f $out/$name.ncu-rep
 }
 run k1_c2      radial_basis  2 python tools/run_config.py 100 100000 0 0 3
+run k1_c3_k2   radial_basis  2 python tools/run_config.py 100 100000 2 0 3
 run k1_c3_k3   radial_basis  2 python tools/run_config.py 100 100000 3 0 3
 run k1_c3_all  radial_basis  2 python tools/run_config.py 100 100000 3 1 3
 run k1_c4      radial_basis  2 python tools/run_config.py 200 10000 0 0 3
