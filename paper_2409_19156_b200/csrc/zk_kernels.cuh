@@ -121,23 +121,48 @@ __device__ __forceinline__ int powset_base(int m) {
 template <int K>
 __device__ __forceinline__ PowSet<K> make_powset_from(dd acc, double rho, int m) {
   PowSet<K> s;
-  const int e_lo = powset_base<K>(m);
-  const int em1 = m - 1 > 0 ? m - 1 : 0;
-  const int em2 = m - 2 > 0 ? m - 2 : 0;
-  const int em3 = m - 3 > 0 ? m - 3 : 0;
   double p_m = 1.0, p_m1 = 1.0, p_m2 = 1.0, p_m3 = 1.0, p_p1 = 0.0, p_p2 = 0.0, p_p3 = 0.0;
+  if (m >= K) {
+    // common case (m is CTA-uniform): acc = rho^(m-K), the window
+    // rho^(m-K) .. rho^(m+K) maps to the named powers statically
+    double w[2 * K + 1];
 #pragma unroll
-  for (int t = 0; t <= 2 * K; ++t) {
-    const int e = e_lo + t;
-    const double v = acc.hi;
-    if (e == m) p_m = v;
-    if (e == em1) p_m1 = v;
-    if (e == em2) p_m2 = v;
-    if (e == em3) p_m3 = v;
-    if (e == m + 1) p_p1 = v;
-    if (e == m + 2) p_p2 = v;
-    if (e == m + 3) p_p3 = v;
-    if (t < 2 * K) acc = dd_mul_d(acc, rho);
+    for (int t = 0; t <= 2 * K; ++t) {
+      w[t] = acc.hi;
+      if (t < 2 * K) acc = dd_mul_d(acc, rho);
+    }
+    p_m = w[K];
+    if constexpr (K >= 1) {
+      p_m1 = w[K - 1];
+      p_p1 = w[K + 1];
+    }
+    if constexpr (K >= 2) {
+      p_m2 = w[K - 2];
+      p_p2 = w[K + 2];
+    }
+    if constexpr (K >= 3) {
+      p_m3 = w[K - 3];
+      p_p3 = w[K + 3];
+    }
+  } else {
+    // m < K: exponents below zero clamp to rho^0 = 1 (zk/evaluate.py:116-117)
+    const int e_lo = powset_base<K>(m);
+    const int em1 = m - 1 > 0 ? m - 1 : 0;
+    const int em2 = m - 2 > 0 ? m - 2 : 0;
+    const int em3 = m - 3 > 0 ? m - 3 : 0;
+#pragma unroll
+    for (int t = 0; t <= 2 * K; ++t) {
+      const int e = e_lo + t;
+      const double v = acc.hi;
+      if (e == m) p_m = v;
+      if (e == em1) p_m1 = v;
+      if (e == em2) p_m2 = v;
+      if (e == em3) p_m3 = v;
+      if (e == m + 1) p_p1 = v;
+      if (e == m + 2) p_p2 = v;
+      if (e == m + 3) p_p3 = v;
+      if (t < 2 * K) acc = dd_mul_d(acc, rho);
+    }
   }
   const double md = static_cast<double>(m);
   s.A0 = p_m;
