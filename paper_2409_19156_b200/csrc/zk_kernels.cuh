@@ -40,14 +40,26 @@ __device__ __forceinline__ dd dd_mul_d(dd a, double b) {
   return dd{s, __dsub_rn(e, __dsub_rn(s, p))};
 }
 
+// a^2 in double-double (2*hi exact): one FMA fewer than dd_mul(a, a)
+__device__ __forceinline__ dd dd_sqr(dd a) {
+  const double p = __dmul_rn(a.hi, a.hi);
+  double e = __fma_rn(a.hi, a.hi, -p);
+  e = __fma_rn(2.0 * a.hi, a.lo, e);
+  const double s = __dadd_rn(p, e);
+  return dd{s, __dsub_rn(e, __dsub_rn(s, p))};
+}
+
 // x**e for integer e >= 0, 0**0 == 1 (zk/evaluate.py:116-117 convention).
+// Left-to-right binary powering: squarings in double-double, and each set bit
+// multiplies by the exact double x (dd_mul_d), ~25 % fewer FP64 ops than the
+// right-to-left form; the result is within a few 2^-104 of x**e, so .hi is
+// the correctly rounded power except at near-ties.
 __device__ __forceinline__ dd dd_pow(double x, int e) {
-  dd r{1.0, 0.0};
-  dd b{x, 0.0};
-  while (e > 0) {
-    if (e & 1) r = dd_mul(r, b);
-    e >>= 1;
-    if (e) b = dd_mul(b, b);
+  if (e <= 0) return dd{1.0, 0.0};
+  dd r{x, 0.0};
+  for (int bit = 30 - __clz(e); bit >= 0; --bit) {
+    r = dd_sqr(r);
+    if ((e >> bit) & 1) r = dd_mul_d(r, x);
   }
   return r;
 }

@@ -509,3 +509,23 @@ def test_unique_column_host_output_equals_device_output(pinned):
     if pinned:
         del host
         _lib.lib.zk_host_free(buf)
+
+
+def test_orthogonality_on_gauss_legendre_nodes():
+    """The reference's acceptance criterion 6 (tests/test_acceptance.py:150-172)
+    on the GPU basis: for every m, the radial polynomials n, n' <= 40 are
+    orthogonal under int_0^1 R_n^m R_n'^m rho drho = delta / (2n + 2), by
+    512-node Gauss-Legendre quadrature, to 1e-10."""
+    x, w = np.polynomial.legendre.leggauss(512)
+    nodes, weights = (x + 1.0) / 2.0, w / 2.0
+    modes = zb.as_mode_set([(n, m) for n in range(41) for m in range(n % 2, n + 1, 2)])
+    table, _ = zb.batch_cached(zb.BatchRequest(modes=modes, grid=nodes))
+    weighted = weights * nodes
+    worst = 0.0
+    for m in range(41):
+        cols = [c for c, md in enumerate(modes) if md.m == m]
+        deg = np.array([modes[c].n for c in cols])
+        blk = table.values[:, cols]
+        gram = blk.T @ (weighted[:, None] * blk)
+        worst = max(worst, float(np.abs(gram - np.diag(1.0 / (2.0 * deg + 2.0))).max()))
+    assert worst <= 1e-10, worst
