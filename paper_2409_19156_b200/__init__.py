@@ -51,6 +51,7 @@ from .series import (
     fit,
     fit_sharded,
     gram,
+    basis_device,
     gram_device,
     series_device,
     series_eval,
@@ -77,7 +78,7 @@ __all__ = [
     "jacobi_argument", "jacobi_chain", "jacobi_derivative_scale", "jacobi_recursion_steps",
     "linear_radial_grid", "make_mode", "radial_at_zero", "radial_grid", "radial_jacobi",
     "rational_radial_grid", "zernike_basis", "zernike_eval", "zernike_radial",
-    "series_eval", "series_device", "gram", "gram_device", "fit", "fit_sharded",
+    "series_eval", "series_device", "basis_device", "gram", "gram_device", "fit", "fit_sharded",
     "solve_normal", "allreduce_normal_equations", "shard_range", "radial_basis_shard",
     "radial_direct", "radial_direct_table", "radial_ztt", "radial_ztt_table",
 ]

@@ -98,6 +98,36 @@ def _torch_ctx(tensor, device):
     return ctx
 
 
+def basis_device(plan_modes, rho, deriv_order: int = 0, theta=None, all_orders: bool = False):
+    """The basis of ``plan_modes`` at the CUDA float64 tensor ``rho`` (and
+    ``theta`` for the 2-D basis), left on the device: a column-major (P, M)
+    tensor view -- or, with ``all_orders``, a list of the k+1 orders 0..k
+    from one kernel sweep -- computed on torch's current stream, no host
+    copy. Values are bitwise those of the numpy entry points. Zero-copy to
+    other frameworks through DLPack (``torch.utils.dlpack.to_dlpack``)."""
+    import torch
+    ms, n, m = _modes(plan_modes)
+    k = _check_order(deriv_order)
+    M, P = len(ms), rho.numel()
+    NO = k + 1 if (all_orders and k > 0) else 1
+    rho = rho.contiguous()
+    theta = theta.contiguous() if theta is not None else None
+    out = torch.empty((NO, M, P), dtype=torch.float64, device=rho.device)
+    if P and M:
+        ctx = _torch_ctx(rho, None)
+        plan = _lib.plan_for(ctx, n, m)
+        if theta is None:
+            rc = _lib.lib.zk_radial_eval(ctx.handle, plan.handle, rho.data_ptr(), P, k,
+                                         int(NO > 1), out.data_ptr(), P, P * M, _lib.ZK_ASYNC)
+        else:
+            rc = _lib.lib.zk_zernike_eval(ctx.handle, plan.handle, rho.data_ptr(),
+                                          theta.data_ptr(), P, k, int(NO > 1), out.data_ptr(),
+                                          P, P * M, _lib.ZK_ASYNC)
+        _lib.check(rc, "zk_radial_eval" if theta is None else "zk_zernike_eval")
+    mats = [out[o].t() for o in range(NO)]
+    return mats if all_orders else mats[0]
+
+
 def gram_device(plan_modes, rho, theta=None, y=None, G=None, Bty=None):
     """Accumulate G += B^T B, Bty += B^T y for CUDA tensors (float64) on the
     tensors' device, on torch's current stream. Returns (G, Bty)."""

@@ -529,3 +529,30 @@ def test_orthogonality_on_gauss_legendre_nodes():
         gram = blk.T @ (weighted[:, None] * blk)
         worst = max(worst, float(np.abs(gram - np.diag(1.0 / (2.0 * deg + 2.0))).max()))
     assert worst <= 1e-10, worst
+
+
+def test_basis_device_stays_on_device_and_matches_numpy_path():
+    """Device-resident basis: torch tensors in, column-major
+    CUDA tensors out, orders 0..k from one sweep; bitwise the numpy path."""
+    modes = zb.full_mode_set(30)
+    rng = np.random.default_rng(33)
+    rho = rng.uniform(size=5000)
+    theta = 2 * np.pi * rng.uniform(size=5000)
+    d_rho = torch.tensor(rho, device="cuda")
+    d_th = torch.tensor(theta, device="cuda")
+    B = zb.basis_device(modes, d_rho, 2)
+    assert B.is_cuda and B.shape == (5000, len(modes)) and B.stride() == (1, 5000)
+    t, _ = zb.evaluate_batch(zb.BatchRequest(modes=modes, grid=rho, deriv_order=2))
+    assert np.array_equal(B.cpu().numpy(), t.values)
+    allo = zb.basis_device(modes, d_rho, 3, all_orders=True)
+    assert len(allo) == 4
+    for k, Bk in enumerate(allo):
+        tk, _ = zb.evaluate_batch(zb.BatchRequest(modes=modes, grid=rho, deriv_order=k))
+        assert np.array_equal(Bk.cpu().numpy(), tk.values), k
+    Z = zb.basis_device(modes, d_rho, 0, theta=d_th)
+    for c in (0, 7, len(modes) - 1):
+        md = modes[c]
+        assert np.array_equal(Z[:, c].cpu().numpy(), zb.zernike_eval(md, rho, theta))
+    from torch.utils import dlpack
+    again = dlpack.from_dlpack(dlpack.to_dlpack(B))
+    assert again.data_ptr() == B.data_ptr()
