@@ -1,0 +1,47 @@
+"""bench.py's driver contract: one JSON line with the required keys, for the
+reference arm (CPU, runs here) and the GPU arm (B200)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+             "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
+             "cpu_baseline"}
+
+
+def _run(args, timeout=600):
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, cwd=ROOT,
+                         capture_output=True, text=True, timeout=timeout)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_json_line():
+    d = _run(["--impl", "reference", "--steps", "2", "--warmup", "1", "--ref-sample", "300"])
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 == d["e2e"]["d2h_bytes_per_step"]
+    assert "workload" in d["config"]
+
+
+@pytest.mark.gpu
+def test_gpu_arm_json_line():
+    d = _run(["--steps", "5", "--warmup", "3", "--no-cpu"])
+    assert BASE_KEYS <= set(d) and {"roofline", "gpu_launches", "clocks"} <= set(d)
+    assert d["gpu_launches"] == 5 and d["n_gpus"] == 1 and d["dtype"] == "f64"
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0.5 < r["frac"] < 1.3
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    e = d["e2e"]
+    assert e["matches_device"] is True and e["value"] > 1e9
+    assert e["d2h_bytes_per_step"] + e["host_filled_bytes_per_step"] == 8 * 100_000 * 5151
+    assert d["oracle_spot_check_max_abs"] <= 1e-11
