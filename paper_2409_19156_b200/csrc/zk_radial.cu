@@ -421,7 +421,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
 }
 
 // Register budgets: the compiler's default heuristic (launch bound without a
-// CTA minimum) lands at 64-80 registers for k <= 1 and 126 for k = 3 single
+// CTA minimum) lands at 64-80 registers for k <= 2 and 98 for k = 3 single
 // order (two CTAs per SM); k = 3 all orders would take ~250 (one CTA per SM,
 // measured 1.5x slower), so it is capped at two CTAs per SM. An explicit
 // minimum of 1 CTA inflates allocation (113-136 registers for k <= 2,
@@ -438,9 +438,8 @@ radial_basis_kernel_2cta(const RadialArgs a) {
   radial_basis_body<K, ALL, ANG, VEC, TMA>(a);
 }
 
-// k = 2, 3, one order: three CTAs per SM (85 registers, a few prologue
-// spills) measured faster than two; the k = 3 all-orders variant is
-// store-bound and slower at three (more spills in its epilogue), so it keeps two.
+// Three CTAs per SM (<= 85 registers): kept for the ZK_MINB=3 experiment
+// (spills for k >= 2 on this build; see launch_t).
 template <int K, bool ALL, bool ANG, int VEC, bool TMA>
 __global__ void __launch_bounds__(kRadialThreads + (TMA ? 32 : 0), 3)
 radial_basis_kernel_3cta(const RadialArgs a) {
@@ -457,14 +456,16 @@ static cudaError_t launch_t(const RadialArgs& a, int grid, size_t smem, cudaStre
   if constexpr (K == 3 && !TMA && VEC <= 2 && ALL) {
     fn = radial_basis_kernel_2cta<K, ALL, ANG, VEC, TMA>;
   } else if constexpr (K >= 2 && !TMA && VEC <= 2 && !ALL) {
-    // single order k = 2: three CTAs per SM (80 registers); k = 3: the
-    // compiler's own budget (126 registers, two CTAs) -- both measured best
-    // with several tiles per CTA (geometry()). ZK_MINB=0/2/3 overrides.
+    // single order k = 2, 3: the compiler's own budget (k = 2: 80 registers,
+    // no spills, three CTAs per SM; k = 3: 98, two) measured best -- forcing
+    // three CTAs spills (k = 2: 0.71 vs 0.65 ms, k = 3: 0.94 vs 0.84 ms at
+    // config 3); both walk several tiles per CTA (geometry()). ZK_MINB=2/3
+    // overrides for experiments.
     static const int minb = [] {
       const char* v = std::getenv("ZK_MINB");
-      return v && *v ? std::atoi(v) : -1;
+      return v && *v ? std::atoi(v) : 0;
     }();
-    const int b = minb >= 0 ? minb : (K == 2 ? 3 : 0);
+    const int b = minb;
     fn = b == 3   ? radial_basis_kernel_3cta<K, ALL, ANG, VEC, TMA>
          : b == 2 ? radial_basis_kernel_2cta<K, ALL, ANG, VEC, TMA>
                   : radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
