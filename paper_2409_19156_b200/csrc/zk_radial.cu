@@ -56,20 +56,19 @@ __device__ __forceinline__ unsigned long long evict_first_policy() {
   return pol;
 }
 
+// No "memory" clobber: the kernel never reads its output, and a clobber would
+// pin the next degree's shared-memory coefficient loads behind every store.
 template <int VEC>
 __device__ __forceinline__ void store_vec(double* dst, const double (&w)[VEC],
                                           unsigned long long pol) {
   if constexpr (VEC == 4) {
     asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst),
-                 "d"(w[0]), "d"(w[1]), "d"(w[2]), "d"(w[3]), "l"(pol)
-                 : "memory");
+                 "d"(w[0]), "d"(w[1]), "d"(w[2]), "d"(w[3]), "l"(pol));
   } else if constexpr (VEC == 2) {
     asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(dst), "d"(w[0]),
-                 "d"(w[1]), "l"(pol)
-                 : "memory");
+                 "d"(w[1]), "l"(pol));
   } else {
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(dst), "d"(w[0]), "l"(pol)
-                 : "memory");
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(dst), "d"(w[0]), "l"(pol));
   }
 }
 
