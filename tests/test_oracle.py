@@ -112,3 +112,22 @@ def test_binary128_oracle_equals_exact_oracle(golden):
     small = [(n, m) for n in range(0, 41) for m in range(-n, n + 1, 2)]
     for k in range(4):
         assert np.array_equal(orc.quad_table(small, pts, k), orc.exact_table(small, pts, k)), k
+
+
+def test_cr_power_variant_differs_only_through_pow():
+    """radial_batch(power=cr_power) -- the GPU's bitwise oracle -- equals the
+    reference port wherever numpy's pow returned the correctly rounded power
+    for every exponent the assembly uses, at every derivative order."""
+    rng = np.random.default_rng(11)
+    modes = [(n, m) for n in range(0, 31) for m in range(-n, n + 1, 2)]
+    pts = rng.uniform(size=60)
+    for k in range(4):
+        a = orc.radial_batch(modes, pts, k)
+        b = orc.radial_batch(modes, pts, k, power=orc.cr_power)
+        for c, (n, m) in enumerate(modes):
+            ma = abs(m)
+            exps = range(max(ma - k, 0), ma + k + 1)
+            same_pow = np.ones(pts.size, bool)
+            for e in exps:
+                same_pow &= orc.numpy_power(pts, e) == orc.cr_power(pts, e)
+            assert np.array_equal(a[same_pow, c], b[same_pow, c]), (n, m, k)
