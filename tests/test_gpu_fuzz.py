@@ -1,0 +1,20 @@
+"""Randomised cross-path fuzzing (tools/fuzz_paths.py) as a regression test:
+host/device inputs and outputs, padding, all orders, 2-D, pinned/pageable,
+duplicated/sparse mode sets -- bitwise the plain device call, which matches
+the oracle on sampled points."""
+
+import importlib.util
+import os
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_fuzzed_paths_agree():
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                        "fuzz_paths.py")
+    spec = importlib.util.spec_from_file_location("fuzz_paths", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.run(seed=20240919, cases=40) == 0
