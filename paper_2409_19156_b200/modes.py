@@ -18,44 +18,53 @@ from . import _lib
 
 
 class ModeError(ValueError):
-    """(n, m) does not index a Zernike polynomial (zk/modes.py:14-15)."""
+    """Base class: the pair does not index a Zernike polynomial (zk/modes.py:14-15)."""
 
 
 class DegreeViolation(ModeError):
-    """n < 0 (zk/modes.py:18-19)."""
+    """Negative radial degree n (zk/modes.py:18-19)."""
 
 
 class BoundViolation(ModeError):
-    """|m| > n (zk/modes.py:22-23)."""
+    """Azimuthal order outside -n..n (zk/modes.py:22-23)."""
 
 
 class ParityViolation(ModeError):
-    """n - |m| odd (zk/modes.py:26-27)."""
+    """n and m of different parity (zk/modes.py:26-27)."""
+
+
+def _violation(n: int, m: int):
+    """The first broken invariant of (n, m) as (exception class, message), or
+    None -- checked in the reference's order: degree, bound, parity."""
+    if n < 0:
+        return DegreeViolation, f"n={n}: the radial degree cannot be negative"
+    if m > n or -m > n:
+        return BoundViolation, f"(n={n}, m={m}): the azimuthal order exceeds the degree"
+    if (n - m) % 2:
+        return ParityViolation, f"(n={n}, m={m}): n and m must have the same parity"
+    return None
 
 
 @dataclass(frozen=True)
 class Mode:
-    """Validated (n, m) pair; invariants of zk/modes.py:37-43."""
+    """A Zernike index (n, m) that satisfies the zk/modes.py:37-43 invariants."""
 
     n: int
     m: int
 
     def __post_init__(self):
-        n, m = self.n, self.m
-        if n < 0:
-            raise DegreeViolation(f"radial degree must be >= 0, got n={n}")
-        if abs(m) > n:
-            raise BoundViolation(f"|m| must not exceed n, got (n={n}, m={m})")
-        if (n - abs(m)) & 1:
-            raise ParityViolation(f"n - |m| must be even, got (n={n}, m={m})")
+        bad = _violation(self.n, self.m)
+        if bad is not None:
+            raise bad[0](bad[1])
 
     @property
     def m_abs(self) -> int:
-        return abs(self.m)
+        return -self.m if self.m < 0 else self.m
 
     @property
     def jacobi_degree(self) -> int:
-        return (self.n - abs(self.m)) // 2
+        """Index j of the backing Jacobi polynomial, (n - |m|) / 2."""
+        return (self.n - self.m_abs) >> 1
 
 
 ModeSet = tuple[Mode, ...]
@@ -72,11 +81,15 @@ def as_mode_set(pairs: Iterable) -> ModeSet:
 
 
 def full_mode_set(resolution: int) -> ModeSet:
-    """zk/modes.py:79-92: n ascending, then m ascending in steps of 2."""
-    resolution = int(resolution)
-    if resolution < 0:
-        raise DegreeViolation(f"resolution must be >= 0, got {resolution}")
-    return tuple(Mode(n, m) for n in range(resolution + 1) for m in range(-n, n + 1, 2))
+    """Every mode up to degree ``resolution``, n ascending then m ascending in
+    steps of 2 (zk/modes.py:79-92); entry n(n+1)/2 + (n+m)/2 is (n, m)."""
+    top = int(resolution)
+    if top < 0:
+        raise DegreeViolation(f"resolution {top} is negative")
+    out = []
+    for n in range(top + 1):
+        out.extend(Mode(n, m) for m in range(-n, n + 1, 2))
+    return tuple(out)
 
 
 def mode_arrays(modes: Sequence[Mode]) -> tuple[np.ndarray, np.ndarray]:
