@@ -122,3 +122,28 @@ def test_empty_requests_need_no_device():
     assert t.values.shape == (0, 10)
     t, c = zb.evaluate_batch(BatchRequest(modes=(), grid=[0.1, 0.2]))
     assert t.values.shape == (2, 0) and c == zb.StepCounter(0, 0)
+
+
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+_mode = st.integers(0, 80).flatmap(lambda n: st.integers(0, n).map(lambda q: (n, -n + 2 * q)))
+
+
+@given(st.lists(_mode, min_size=0, max_size=60), st.integers(0, 3))
+@settings(max_examples=150, deadline=None, derandomize=True)
+def test_native_plan_and_counters_on_arbitrary_requests(pairs, k):
+    """Native planner == the reference algorithm (oracle port of zk/modes.py:
+    108-125, zk/batch.py:69-94) on arbitrary requests, and the cached strategy
+    never needs more recursion steps than the independent one (reference
+    tests/test_batch.py: counter dominance)."""
+    import zk_oracle as orc
+    ms = zb.as_mode_set(pairs)
+    plan = zb.dedup_plan(ms)
+    keys, scatter = orc.unique_and_scatter([(md.n, md.m) for md in ms])
+    assert list(plan.unique_keys) == [tuple(x) for x in keys]
+    assert list(plan.scatter) == list(scatter)
+    c = zb.cached_step_counter(plan, k)
+    i = zb.independent_step_counter(plan, k)
+    assert (c.recursion_steps, c.chain_count) == orc.step_counts(keys, k, True)
+    assert (i.recursion_steps, i.chain_count) == orc.step_counts(keys, k, False)
+    assert c.recursion_steps <= i.recursion_steps and c.chain_count <= i.chain_count
