@@ -6,7 +6,6 @@ installed names return the reference's own result types with GPU values."""
 import os
 import sys
 
-import numpy as np
 import pytest
 
 REF = "/root/reference/pkg/src"
