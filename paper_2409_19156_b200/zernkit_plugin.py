@@ -38,7 +38,7 @@ _TARGETS = {
 
 def _wrappers(zk):
     from . import _lib
-    from .evaluate import basis_matrix
+    from .evaluate import basis_matrix, parallel_devices
 
     ref_eval = importlib.import_module(zk.__name__ + ".evaluate")
     ref_batch = importlib.import_module(zk.__name__ + ".batch")
@@ -77,9 +77,12 @@ def _wrappers(zk):
                            int(deriv_order), theta=theta)
         return col[:, 0].copy()
 
-    def _run(request, shared):
+    def _run(request, shared, parallel):
+        # parallel=True: the reference's thread pool (zk/batch.py:136-141)
+        # becomes point shards over every visible GPU; bitwise the same values
         n, m = _arrays(request.modes)
-        values = basis_matrix(n, m, request.grid, request.deriv_order)
+        values = basis_matrix(n, m, request.grid, request.deriv_order,
+                              devices=parallel_devices() if parallel else None)
         steps, chains = _lib.step_counters(n, m, request.deriv_order, shared)
         table = ref_tables.EvalMatrix(values=values, modes=request.modes,
                                       deriv_order=request.deriv_order)
@@ -88,13 +91,13 @@ def _wrappers(zk):
     def batch_cached(request, parallel=False):
         if request.strategy != "cached":
             raise ValueError(f"request strategy is {request.strategy!r}, expected 'cached'")
-        return _run(request, True)
+        return _run(request, True, parallel)
 
     def batch_independent(request, parallel=False):
         if request.strategy != "independent":
             raise ValueError(
                 f"request strategy is {request.strategy!r}, expected 'independent'")
-        return _run(request, False)
+        return _run(request, False, parallel)
 
     def evaluate_batch(request, parallel=False):
         if request.strategy == "cached":
