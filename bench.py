@@ -14,8 +14,10 @@ Arms
 Timing: W warm-up steps, then K steps bracketed by barrier + synchronize,
 CUDA events on the launching stream, max over ranks. The 4.12 GB output is
 32x the 126 MB L2, so no flush is needed between steps. `e2e` repeats the
-metric through the same C ABI with host (pinned) buffers: H2D of the grid and
-D2H of the whole basis inside the timed region.
+metric through the same C ABI with host (pinned) buffers: every step copies
+the grid H2D and lands the whole 4.12 GB basis in host memory (the unique
+(n,|m|) columns over PCIe, the repeated ones filled on the host) inside the
+timed region.
 """
 
 from __future__ import annotations
