@@ -138,9 +138,11 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho,
 /* ---- K4: least-squares normal equations, accumulated -------------------
  * G (M x M, column-major, full symmetric) += B^T B and Bty (M) += B^T y over
  * the P points, B the 2-D basis (theta != NULL) or radial basis (theta ==
- * NULL). G/Bty are device buffers the caller zeroes before the first call
- * (accumulation lets a caller stream points through in chunks; the
- * cross-GPU sum is an allreduce of G and Bty). y may be NULL (skip Bty). */
+ * NULL). G/Bty are device buffers (host buffers with ZK_HOST_OUTPUT) that the
+ * caller zeroes before the first call (accumulation lets a caller stream
+ * points through in chunks; the cross-GPU sum is an allreduce of G and Bty).
+ * y may be NULL (skip Bty). Sums run in a fixed order: deterministic, and G
+ * exactly symmetric. */
 int zk_gram_accumulate(zk_ctx* ctx, const zk_plan* plan, const double* rho,
                        const double* theta, int64_t P, const double* y,
                        double* G, double* Bty, uint32_t flags);
