@@ -114,3 +114,8 @@ def test_bench_records(tmp_path):
     for n in (10, 20, 30):
         assert by[("cached", n)] <= by[("independent", n)]
         assert by[("cached", n)] == sum(max(0, (n - a) // 2 - 1) for a in range(n + 1))
+
+
+def test_precision_points_to_the_reference():
+    res = CliRunner().invoke(main, ["precision", "--n-max", "10"])
+    assert res.exit_code == 2 and "reference" in res.output
