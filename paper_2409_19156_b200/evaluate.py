@@ -140,7 +140,7 @@ def radial_jacobi(n: int, m_abs: int, grid, deriv_order: int = 0) -> np.ndarray:
     rho = radial_grid(grid)
     col = basis_matrix(np.array([mode.n], np.int32), np.array([mode.m_abs], np.int32), rho,
                        int(deriv_order))
-    return col[:, 0].copy()
+    return col[:, 0]  # the (P, 1) result is one contiguous column: no copy
 
 
 def zernike_eval(mode: Mode, grid, angles, deriv_order: int = 0) -> np.ndarray:
@@ -154,7 +154,7 @@ def zernike_eval(mode: Mode, grid, angles, deriv_order: int = 0) -> np.ndarray:
     _check_order(deriv_order)
     col = basis_matrix(np.array([mode.n], np.int32), np.array([mode.m], np.int32), rho,
                        int(deriv_order), theta=theta)
-    return col[:, 0].copy()
+    return col[:, 0]  # the (P, 1) result is one contiguous column: no copy
 
 
 def radial_at_zero(n: int, m: int) -> float:

@@ -22,7 +22,7 @@ from collections import OrderedDict
 
 import numpy as np
 
-MIN_POOLED_BYTES = 16 << 20
+MIN_POOLED_BYTES = 1 << 20
 
 
 class _Lease:

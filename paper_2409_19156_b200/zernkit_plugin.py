@@ -62,7 +62,7 @@ def _wrappers(zk):
         rho = ref_tables.radial_grid(grid)
         col = basis_matrix(np.array([mode.n], np.int32), np.array([mode.m_abs], np.int32),
                            rho, int(deriv_order))
-        return col[:, 0].copy()
+        return col[:, 0]  # the (P, 1) result is one contiguous column: no copy
 
     def zernike_eval(mode, grid, angles, deriv_order=0):
         rho = ref_tables.radial_grid(grid)
@@ -75,7 +75,7 @@ def _wrappers(zk):
             raise ValueError(f"derivative order must be 0..3, got {deriv_order}")
         col = basis_matrix(np.array([mode.n], np.int32), np.array([mode.m], np.int32), rho,
                            int(deriv_order), theta=theta)
-        return col[:, 0].copy()
+        return col[:, 0]  # the (P, 1) result is one contiguous column: no copy
 
     def _run(request, shared, parallel):
         # parallel=True: the reference's thread pool (zk/batch.py:136-141)
