@@ -15,7 +15,8 @@ reference's public API, unmodified:
 * ``c4_*``  full set n<=200 on a subsample of linear_radial_grid(10**4), with
   the reference's exact oracle on the same points (config 4);
 * ``c5_*``  2-D basis n<=60 at disc points (config 5) via per-mode
-  ``zernike_eval`` (reference zk/cli.py:438-440 pattern) and f = B @ c;
+  ``zernike_eval`` (reference zk/cli.py:438-440 pattern), derivative orders
+  0..3, and f = B @ c;
 * ``idx_*`` mode indexing: full_mode_set, dedup plans of mixed requests,
   step counters.
 """
@@ -116,6 +117,11 @@ def main():
     for c, md in enumerate(modes):
         B1[:, c] = zk.zernike_eval(md, rho, theta, 1)
     g["c5_B_k1"] = B1
+    for k in (2, 3):  # higher radial-derivative orders of the 2-D basis
+        Bk = np.empty((npts, len(modes)), order="F")
+        for c, md in enumerate(modes):
+            Bk[:, c] = zk.zernike_eval(md, rho, theta, k)
+        g[f"c5_B_k{k}"] = Bk
 
     # ---- mode indexing
     fm = zk.full_mode_set(200)
