@@ -17,6 +17,7 @@ reference's public API, unmodified:
 * ``c5_*``  2-D basis n<=60 at disc points (config 5) via per-mode
   ``zernike_eval`` (reference zk/cli.py:438-440 pattern), derivative orders
   0..3, and f = B @ c;
+* ``base_*`` the float baselines radial_direct (k <= 2) and radial_ztt_table;
 * ``idx_*`` mode indexing: full_mode_set, dedup plans of mixed requests,
   step counters.
 """
@@ -148,6 +149,17 @@ def main():
             vals, _ = batch(zk, modes_r, grid, k)
             g[f"idx_req{r}_k{k}"] = vals
     g["idx_req_grid"] = zk.linear_radial_grid(33)
+
+    # ---- the float baselines (zk/evaluate.py:189-247) at mixed points
+    brng = np.random.default_rng(7)
+    bpts = np.concatenate([[0.0, 1.0, 0.5], brng.uniform(0.0, 1.0, size=29)])
+    bmodes = [(n, m) for n in range(0, 41, 3) for m in range(n % 2, n + 1, 4)]
+    g["base_pts"] = bpts
+    g["base_modes"] = np.array(bmodes, dtype=np.int32)
+    for k in (0, 1, 2):
+        g[f"base_direct_k{k}"] = np.stack(
+            [zk.radial_direct(n, m, bpts, k) for n, m in bmodes], axis=1)
+    g["base_ztt"] = zk.radial_ztt_table(zk.as_mode_set(bmodes), bpts)
 
     # ---- the reference's accuracy study (zk/cli.py:98-130), all methods, k <= 1
     from zernkit.cli import METHODS, run_accuracy

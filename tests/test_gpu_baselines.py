@@ -82,3 +82,20 @@ def test_double_double_reference_equals_exact_oracle(golden):
         ex = orc.exact_table_rational(small, pts, k)
         assert np.mean(ref == ex) > 0.99, k
         assert np.abs(ref - ex).max() <= 1e-14 * max(1.0, np.abs(ex).max()), k
+
+
+def test_baselines_match_reference_golden(golden):
+    """GPU float baselines against outputs of the reference itself
+    (tests/golden: radial_direct k <= 2, radial_ztt_table), within the
+    baselines' own rounding (column-scaled 1e-13; the direct sum is unstable
+    by design, so high-degree columns are compared relative to their size)."""
+    pts = golden["base_pts"]
+    modes = [tuple(int(x) for x in r) for r in golden["base_modes"]]
+    for k in (0, 1, 2):
+        ref = golden[f"base_direct_k{k}"]
+        got = np.stack([zb.radial_direct(n, m, pts, k) for n, m in modes], axis=1)
+        scale = np.maximum(1.0, np.abs(ref).max(axis=0))
+        assert (np.abs(got - ref).max(axis=0) <= 1e-13 * scale).all(), k
+    ref = golden["base_ztt"]
+    got = zb.radial_ztt_table(zb.as_mode_set(modes), pts)
+    assert np.abs(got - ref).max() <= 1e-14

@@ -132,3 +132,15 @@ def test_cr_power_variant_differs_only_through_pow():
             for e in exps:
                 same_pow &= orc.numpy_power(pts, e) == orc.cr_power(pts, e)
             assert np.array_equal(a[same_pow, c], b[same_pow, c]), (n, m, k)
+
+
+def test_float_baselines_match_the_reference(golden):
+    """The oracle's restatement of the reference's float baselines
+    (zk/evaluate.py:189-247: direct Horner sum, Zernike three-term table) is
+    bitwise the reference's output on the generating host."""
+    pts = golden["base_pts"]
+    modes = [tuple(int(x) for x in r) for r in golden["base_modes"]]
+    for k in (0, 1, 2):
+        got = np.stack([orc.direct_single(n, m, pts, k) for n, m in modes], axis=1)
+        assert _ulp_close(got, golden[f"base_direct_k{k}"]), k
+    assert _ulp_close(orc.ztt_table(modes, pts), golden["base_ztt"])
