@@ -17,6 +17,7 @@ reference's public API, unmodified:
 * ``c5_*``  2-D basis n<=60 at disc points (config 5) via per-mode
   ``zernike_eval`` (reference zk/cli.py:438-440 pattern), derivative orders
   0..3, and f = B @ c;
+* ``chain_*`` jacobi_chain rows for shifted (alpha, beta), x in [-1, 1];
 * ``base_*`` the float baselines radial_direct (k <= 2) and radial_ztt_table;
 * ``idx_*`` mode indexing: full_mode_set, dedup plans of mixed requests,
   step counters.
@@ -149,6 +150,15 @@ def main():
             vals, _ = batch(zk, modes_r, grid, k)
             g[f"idx_req{r}_k{k}"] = vals
     g["idx_req_grid"] = zk.linear_radial_grid(33)
+
+    # ---- jacobi_chain (zk/evaluate.py:36-76) for shifted parameters
+    crng = np.random.default_rng(8)
+    cx = np.concatenate([[-1.0, 1.0, 0.0], crng.uniform(-1.0, 1.0, size=21)])
+    g["chain_x"] = cx
+    chain_cases = [(0, 0, 0), (1, 3, 0), (40, 0, 0), (25, 7, 1), (30, 12, 2), (18, 50, 3)]
+    g["chain_cases"] = np.array(chain_cases, dtype=np.int32)
+    for jm, al, be in chain_cases:
+        g[f"chain_{jm}_{al}_{be}"] = zk.jacobi_chain(jm, al, be, cx)
 
     # ---- the float baselines (zk/evaluate.py:189-247) at mixed points
     brng = np.random.default_rng(7)

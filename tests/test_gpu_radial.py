@@ -557,3 +557,11 @@ def test_basis_device_stays_on_device_and_matches_numpy_path():
     from torch.utils import dlpack
     again = dlpack.from_dlpack(dlpack.to_dlpack(B))
     assert again.data_ptr() == B.data_ptr()
+
+
+def test_jacobi_chain_export_matches_reference_golden(golden):
+    """zk_jacobi_chain (GPU) == the reference's jacobi_chain, bitwise."""
+    x = golden["chain_x"]
+    for jm, al, be in golden["chain_cases"]:
+        got = zb.jacobi_chain(int(jm), int(al), int(be), x)
+        assert np.array_equal(got, golden[f"chain_{jm}_{al}_{be}"]), (jm, al, be)

@@ -144,3 +144,12 @@ def test_float_baselines_match_the_reference(golden):
         got = np.stack([orc.direct_single(n, m, pts, k) for n, m in modes], axis=1)
         assert _ulp_close(got, golden[f"base_direct_k{k}"]), k
     assert _ulp_close(orc.ztt_table(modes, pts), golden["base_ztt"])
+
+
+def test_jacobi_chain_matches_the_reference(golden):
+    """oracle jacobi_chain == zk/evaluate.py:36-76 output, bitwise (pure
+    +,-,*,/ in the reference's order: host independent)."""
+    x = golden["chain_x"]
+    for jm, al, be in golden["chain_cases"]:
+        assert np.array_equal(orc.jacobi_chain(int(jm), int(al), int(be), x),
+                              golden[f"chain_{jm}_{al}_{be}"]), (jm, al, be)
