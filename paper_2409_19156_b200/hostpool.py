@@ -50,7 +50,7 @@ class ResultPool:
         self.cap = cap_bytes
         self.free: OrderedDict[int, list[np.ndarray]] = OrderedDict()
         self.held = 0
-        self.lock = threading.Lock()
+        self.lock = threading.RLock()  # re-entrant: a GC-triggered release may run inside take()
 
     def take(self, count: int) -> np.ndarray:
         """A 1-D float64 array of ``count`` elements (contents undefined)."""
