@@ -45,3 +45,18 @@ def test_gpu_arm_json_line():
     assert e["matches_device"] is True and e["value"] > 1e9
     assert e["d2h_bytes_per_step"] + e["host_filled_bytes_per_step"] == 8 * 100_000 * 5151
     assert d["oracle_spot_check_max_abs"] <= 1e-11
+
+
+def test_reference_arm_under_torchrun_prints_once():
+    """N > 1 (driver launches the reference arm through torchrun too): rank 0
+    alone runs and prints; the other ranks exit 0 without work."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29561",
+           os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+           "--warmup", "0", "--ref-sample", "200"]
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
