@@ -60,3 +60,22 @@ def test_reference_arm_under_torchrun_prints_once():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+@pytest.mark.gpu
+def test_gpu_arm_multi_rank_path_on_one_gpu():
+    """The torchrun path of the GPU arm (barriers, max-over-ranks timing,
+    rank-0 line) with two ranks sharing the one GPU through gloo -- a
+    functional check of the code the driver's N-GPU runs take (NCCL itself
+    needs one device per rank)."""
+    env = dict(os.environ, ZK_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29563",
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+           "--no-e2e"]
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_points"] == 200_000 and d["gpu_launches"] == 3
