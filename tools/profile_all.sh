@@ -28,3 +28,8 @@ run k2_c5      radial_basis  2 python tools/run_config.py 60 1000000 0 0 3 1
 run k3_series  series_kernel 2 python tools/run_series.py
 run k4_syrk    syrk_partial  0 python tools/run_gram.py
 run k4_reduce  syrk_reduce   0 python tools/run_gram.py
+run k3_series_dmma series_dmma  2 python tools/run_misc.py dmma
+run x_chain    jacobi_chain  2 python tools/run_misc.py chain
+run x_direct   direct_kernel 2 python tools/run_misc.py direct
+run x_ztt      ztt_kernel    2 python tools/run_misc.py ztt
+run x_dd       radial_dd     2 python tools/run_misc.py dd
