@@ -81,6 +81,10 @@ int zk_ctx_destroy(zk_ctx* ctx);
 /* Launch on a caller-owned cudaStream_t (passed as void*); NULL = ctx stream. */
 int zk_ctx_set_stream(zk_ctx* ctx, void* stream);
 int zk_ctx_synchronize(zk_ctx* ctx);
+/* Wait for the ctx's work, then free its cached device scratch and pinned
+ * bounce buffers (they are re-allocated on demand; for long-running
+ * services that want the memory back between bursts). */
+int zk_ctx_release_buffers(zk_ctx* ctx);
 /* Number of kernels this ctx launched since creation (bench accounting). */
 int zk_ctx_launch_count(const zk_ctx* ctx, int64_t* count);
 

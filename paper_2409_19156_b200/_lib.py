@@ -50,6 +50,7 @@ SIGNATURES = {
     "zk_ctx_destroy": (c_int, [c_void_p]),
     "zk_ctx_set_stream": (c_int, [c_void_p, c_void_p]),
     "zk_ctx_synchronize": (c_int, [c_void_p]),
+    "zk_ctx_release_buffers": (c_int, [c_void_p]),
     "zk_ctx_launch_count": (c_int, [c_void_p, _i64p]),
     "zk_plan_describe": (c_int, [_i32p, _i32p, c_int64, _i32p, _i32p, _i32p, _i64p]),
     "zk_step_counters": (c_int, [_i32p, _i32p, c_int64, c_int, c_int, _i64p, _i64p]),
@@ -146,6 +147,10 @@ class Context:
         c = c_int64(0)
         check(lib.zk_ctx_launch_count(self.handle, ctypes.byref(c)), "zk_ctx_launch_count")
         return c.value
+
+    def release_buffers(self) -> None:
+        """Free the context's cached scratch and pinned bounce buffers."""
+        check(lib.zk_ctx_release_buffers(self.handle), "zk_ctx_release_buffers")
 
     def set_stream(self, stream_ptr: int | None) -> None:
         check(lib.zk_ctx_set_stream(self.handle, c_void_p(stream_ptr or 0)), "zk_ctx_set_stream")

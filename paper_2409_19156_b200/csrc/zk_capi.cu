@@ -677,6 +677,23 @@ int zk_ctx_synchronize(zk_ctx* ctx) {
   return ZK_OK;
 }
 
+int zk_ctx_release_buffers(zk_ctx* ctx) {
+  if (!ctx) return fail(ZK_EINVAL, "null ctx");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  ZK_CUDA(cudaSetDevice(ctx->device));
+  ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int s = 0; s < 2; ++s) {
+    ZK_CUDA(cudaStreamSynchronize(ctx->pipe[s]));
+    if (ctx->scratch[s]) cudaFree(ctx->scratch[s]);
+    ctx->scratch[s] = nullptr;
+    ctx->scratch_bytes[s] = 0;
+    if (ctx->hbounce[s]) cudaFreeHost(ctx->hbounce[s]);
+    ctx->hbounce[s] = nullptr;
+    ctx->hbounce_bytes[s] = 0;
+  }
+  return ZK_OK;
+}
+
 int zk_ctx_launch_count(const zk_ctx* ctx, int64_t* count) {
   if (!ctx || !count) return fail(ZK_EINVAL, "null argument");
   *count = ctx->launches;

@@ -565,3 +565,14 @@ def test_jacobi_chain_export_matches_reference_golden(golden):
     for jm, al, be in golden["chain_cases"]:
         got = zb.jacobi_chain(int(jm), int(al), int(be), x)
         assert np.array_equal(got, golden[f"chain_{jm}_{al}_{be}"]), (jm, al, be)
+
+
+def test_release_buffers_then_reuse():
+    """zk_ctx_release_buffers frees the cached scratch / pinned buffers; the
+    next host-output call re-allocates them and gives the same values."""
+    modes = zb.full_mode_set(40)
+    grid = np.random.default_rng(3).uniform(size=30_000)
+    a, _ = zb.evaluate_batch(zb.BatchRequest(modes=modes, grid=grid))
+    _lib.context().release_buffers()
+    b, _ = zb.evaluate_batch(zb.BatchRequest(modes=modes, grid=grid))
+    assert np.array_equal(a.values, b.values)
