@@ -6,6 +6,11 @@
 // assembly, same angular factor), and folded into NC running sums per point
 // instead of being stored: the 15 GB basis of config 5 never exists.
 //
+// The angular factors are the one exception to "exactly as K2": consecutive
+// groups advance cos/sin(alpha theta) by rotation through theta, re-anchored
+// on the exact sincos(fl(alpha theta)) at least every 8 alpha-steps (~1e-15
+// relative; measured at config 5: |f - B c| <= 1.5e-15 sum|B||c|).
+//
 // Decomposition: one CTA owns a tile of kThreads*VEC points and walks every
 // alpha group of the plan in ascending alpha; each thread carries VEC points.
 // Per group, the recursion coefficients / prefactors / row pointers are
@@ -90,6 +95,20 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
     pw_acc[v] = dd{1.0, 0.0};
   }
   int e_cur = 0;
+  // angular factors cos/sin(alpha theta) for the ascending groups: exact
+  // sincos(fl(alpha theta)) at an anchor, then rotations by theta for small
+  // alpha steps (<= 4 per group, <= 8 since the anchor: ~1e-15 relative,
+  // far inside the series tolerance); saves most of the per-group sincos
+  double c1[kVec], s1[kVec], cs_a[kVec], sn_a[kVec];
+  int a_cur = -1, since = 0;
+#pragma unroll
+  for (int v = 0; v < kVec; ++v) {
+    c1[v] = 1.0;
+    s1[v] = 0.0;
+    cs_a[v] = 1.0;
+    sn_a[v] = 0.0;
+    if (ANG) sincos(th[v], &s1[v], &c1[v]);
+  }
   double acc[NC][kVec];
 #pragma unroll
   for (int c = 0; c < NC; ++c)
@@ -133,16 +152,32 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
     // rho powers: advance the double-double accumulator to rho^base (alpha ascends)
     const int e_lo = powset_base<K>(alpha);
     PowSet<K> pw[kVec];
-    double cs_a[kVec], sn_a[kVec];
 #pragma unroll
     for (int v = 0; v < kVec; ++v) {
       if (e_lo > e_cur) pw_acc[v] = dd_mul(pw_acc[v], dd_pow(rho[v], e_lo - e_cur));
       pw[v] = make_powset_from<K>(pw_acc[v], rho[v], alpha);
-      cs_a[v] = 1.0;
-      sn_a[v] = 0.0;
-      if (ANG) sincos(__dmul_rn(static_cast<double>(alpha), th[v]), &sn_a[v], &cs_a[v]);
     }
     e_cur = e_lo > e_cur ? e_lo : e_cur;
+    if constexpr (ANG) {
+      const int step = alpha - a_cur;  // CTA-uniform
+      if (a_cur >= 0 && step <= 4 && since + step <= 8) {
+        for (int t = 0; t < step; ++t) {
+#pragma unroll
+          for (int v = 0; v < kVec; ++v) {
+            const double c = fma(cs_a[v], c1[v], -sn_a[v] * s1[v]);
+            sn_a[v] = fma(sn_a[v], c1[v], cs_a[v] * s1[v]);
+            cs_a[v] = c;
+          }
+        }
+        since += step;
+      } else {
+#pragma unroll
+        for (int v = 0; v < kVec; ++v)
+          sincos(__dmul_rn(static_cast<double>(alpha), th[v]), &sn_a[v], &cs_a[v]);
+        since = 0;
+      }
+      a_cur = alpha;
+    }
 
     // per-group sums: the angular factors are constant over a group, so they
     // multiply the group's two partial sums once (2 FMAs per key instead of 3)
