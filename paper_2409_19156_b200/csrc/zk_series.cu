@@ -1,12 +1,12 @@
 // K3: series evaluation f = B c without materialising B.
 //
 // f[p, v] = sum_col c[col, v] * Z_col(p), Z the 2-D basis (radial x cos/sin,
-// zk/evaluate.py:259-274) or the radial basis, derivative order K. The basis
-// values are produced exactly as K1/K2 produce them (same recursion, same
-// assembly, same angular factor), and folded into NC running sums per point
-// instead of being stored: the 15 GB basis of config 5 never exists.
+// zk/evaluate.py:259-274) or the radial basis, derivative order K. The radial
+// values are produced exactly as K1 produces them (same recursion, same
+// assembly), and folded into NC running sums per point instead of being
+// stored: the 15 GB basis of config 5 never exists.
 //
-// The angular factors are the one exception to "exactly as K2": consecutive
+// The angular factors are the one departure from K2's arithmetic: consecutive
 // groups advance cos/sin(alpha theta) by rotation through theta, re-anchored
 // on the exact sincos(fl(alpha theta)) at least every 8 alpha-steps (~1e-15
 // relative; measured at config 5: |f - B c| <= 1.5e-15 sum|B||c|).
