@@ -288,7 +288,7 @@ void column_copy(double* dst, const double* src, size_t n) {
 
 
 Geometry geometry(const zk_ctx* ctx, const zk_plan* plan, int64_t P, int K, bool all, int vec,
-                  bool tma) {
+                  bool tma, bool coef_global = false) {
   Geometry g{};
   g.vec = vec;
   const int64_t tile_pts = int64_t(zk::kRadialThreads) * g.vec;
@@ -312,7 +312,7 @@ Geometry geometry(const zk_ctx* ctx, const zk_plan* plan, int64_t P, int K, bool
   g.col_cap = plan->host.max_group_cols;
   auto smem_for = [&]() {
     return zk::radial_smem_bytes(K, all, g.vec, g.tma, g.stage_slots, plan->host.max_jmax,
-                                 g.col_cap);
+                                 g.col_cap, coef_global);
   };
   g.smem = smem_for();
   if (g.smem > ctx->max_smem && g.tma) {
@@ -345,8 +345,16 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
   }
   const bool tma = !force_scalar && vec >= 2 && env_int("ZK_TMA", 0) != 0;
   Geometry geo = geometry(ctx, plan, P, K, all, vec, tma);
+  bool coef_global = false;
+  if (geo.smem > ctx->max_smem) {
+    // very long chains: coefficient tables stay in global memory (scalar-store
+    // fallback kernel); only the column offsets and row pointers are staged
+    coef_global = true;
+    vec = 1;
+    geo = geometry(ctx, plan, P, K, all, vec, false, true);
+  }
   if (geo.smem > ctx->max_smem)
-    return fail(ZK_EINVAL, "mode set too large for the shared-memory coefficient stage "
+    return fail(ZK_EINVAL, "mode set too large for the shared-memory column stage "
                            "(highest jacobi degree " + std::to_string(plan->host.max_jmax) + ")");
   zk::RadialArgs a{};
   a.groups = plan->groups;
@@ -366,6 +374,7 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
   a.tiles_per_chunk = geo.tiles_per_chunk;
   a.col_cap = geo.col_cap;
   a.stage_slots = geo.stage_slots;
+  a.coef_global = coef_global ? 1 : 0;
   cudaError_t e = zk::launch_radial(a, K, all, theta != nullptr, geo.vec, geo.tma, geo.grid, geo.smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "radial kernel launch");
   ctx->launches += 1;

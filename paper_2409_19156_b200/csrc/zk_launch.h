@@ -29,11 +29,13 @@ struct RadialArgs {
   int tiles_per_chunk;
   int col_cap;            // column offsets staged in smem when a group has <= col_cap
   int stage_slots;        // (column, order) slots per TMA staging stage
+  int coef_global;        // 1: read the group's coefficient tables from global memory
+                          //    (L1-cached broadcasts) instead of staging them in smem
 };
 
 int radial_stages(bool all);
 size_t radial_smem_bytes(int K, bool all, int vec, bool tma, int stage_slots, int max_jmax,
-                         int col_cap);
+                         int col_cap, bool coef_global = false);
 cudaError_t launch_radial(const RadialArgs& a, int K, bool all, bool ang, int vec, bool tma,
                           int grid, size_t smem, cudaStream_t st);
 

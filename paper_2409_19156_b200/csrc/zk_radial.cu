@@ -165,7 +165,7 @@ struct Thread {
   }
 };
 
-template <int K, bool ALL, bool ANG, int VEC, bool TMA>
+template <int K, bool ALL, bool ANG, int VEC, bool TMA, bool GC = false>
 __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
   using T = Thread<K, ALL, ANG, VEC>;
   constexpr int NO = T::NO;
@@ -188,17 +188,21 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
   unsigned long long* bar_empty = bar_full + S;
   double* s_stage = reinterpret_cast<double*>(smem_raw + 128);
   const int maxc = a.stage_slots;
+  // GC: very long chains (the coefficient tables do not fit in shared
+  // memory) read them from global memory -- warp-uniform, L1-cached loads
   ChainCoef* s_coef = reinterpret_cast<ChainCoef*>(s_stage + (TMA ? S * maxc * TP : 0));
-  AsmCoef* s_asm = reinterpret_cast<AsmCoef*>(s_coef + (K + 1) * nj);
-  long long* s_off = reinterpret_cast<long long*>(s_asm + (K > 0 ? nj : 0));
+  AsmCoef* s_asm = reinterpret_cast<AsmCoef*>(s_coef + (GC ? 0 : (K + 1) * nj));
+  long long* s_off = reinterpret_cast<long long*>(s_asm + (GC || K == 0 ? 0 : nj));
+  const ChainCoef* coefp = GC ? a.coef + g.coef_off : s_coef;
+  const AsmCoef* asmp = GC ? a.asmc + g.asm_off : s_asm;
   int* s_row = reinterpret_cast<int*>(s_off + g.ncols);
   const int row_base = __ldg(a.rowptr + g.row0);
   {
     const double* src = reinterpret_cast<const double*>(a.coef + g.coef_off);
     double* dst = reinterpret_cast<double*>(s_coef);
-    const int n_coef = (K + 1) * nj * 6;
+    const int n_coef = GC ? 0 : (K + 1) * nj * 6;
     for (int t = tid; t < n_coef; t += nthreads) dst[t] = __ldg(src + t);
-    if (K > 0) {
+    if (K > 0 && !GC) {
       const double* asrc = reinterpret_cast<const double*>(a.asmc + g.asm_off);
       double* adst = reinterpret_cast<double*>(s_asm);
       for (int t = tid; t < nj * 8; t += nthreads) adst[t] = __ldg(asrc + t);
@@ -293,7 +297,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
       const int r_hi = s_row[j + 1];
       if (r_lo == r_hi) return;  // CTA-uniform
       AsmCoef ac;
-      if constexpr (K > 0) ac = load_asm(s_asm + j);
+      if constexpr (K > 0) ac = load_asm(asmp + j);
       double val[NO][VEC];
       th.template values<decltype(steady)::value, decltype(par)::value>(j, ac, chs, val);
       if (!use_tma) {
@@ -374,7 +378,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
             th.cur[i][v] = jacobi_p1(a1, ab2, th.u[v]);
           }
         } else if (d >= 2) {
-          const ChainCoef c = load_coef(s_coef + i * nj + d);
+          const ChainCoef c = load_coef(coefp + i * nj + d);
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
             const double nx = jacobi_step(c, th.u[v], th.cur[i][v], th.prev[i][v]);
@@ -394,14 +398,14 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
     for (; j + 1 <= jmax; j += 2) {
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = load_coef(s_coef + i * nj + (j - i));
+        const ChainCoef c = load_coef(coefp + i * nj + (j - i));
 #pragma unroll
         for (int v = 0; v < VEC; ++v) B[i][v] = jacobi_step(c, th.u[v], A[i][v], B[i][v]);
       }
       emit(j, B, std::true_type{}, std::integral_constant<int, K % 2>{});
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = load_coef(s_coef + i * nj + (j + 1 - i));
+        const ChainCoef c = load_coef(coefp + i * nj + (j + 1 - i));
 #pragma unroll
         for (int v = 0; v < VEC; ++v) A[i][v] = jacobi_step(c, th.u[v], B[i][v], A[i][v]);
       }
@@ -410,7 +414,7 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
     if (j <= jmax) {
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = load_coef(s_coef + i * nj + (j - i));
+        const ChainCoef c = load_coef(coefp + i * nj + (j - i));
 #pragma unroll
         for (int v = 0; v < VEC; ++v) B[i][v] = jacobi_step(c, th.u[v], A[i][v], B[i][v]);
       }
@@ -425,10 +429,10 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
 // measured 1.5x slower), so it is capped at two CTAs per SM. An explicit
 // minimum of 1 CTA inflates allocation (113-136 registers for k <= 2,
 // measured slower) -- hence separate kernel wrappers.
-template <int K, bool ALL, bool ANG, int VEC, bool TMA>
+template <int K, bool ALL, bool ANG, int VEC, bool TMA, bool GC = false>
 __global__ void __launch_bounds__(kRadialThreads + (TMA ? 32 : 0))
 radial_basis_kernel(const RadialArgs a) {
-  radial_basis_body<K, ALL, ANG, VEC, TMA>(a);
+  radial_basis_body<K, ALL, ANG, VEC, TMA, GC>(a);
 }
 
 template <int K, bool ALL, bool ANG, int VEC, bool TMA>
@@ -491,6 +495,16 @@ static cudaError_t launch_v(const RadialArgs& a, int vec, bool tma, int grid, si
       return tma ? launch_t<K, ALL, ANG, 2, true>(a, grid, smem, st)
                  : launch_t<K, ALL, ANG, 2, false>(a, grid, smem, st);
     default:
+      if (a.coef_global) {  // long-chain fallback (coefficients from global memory)
+        void (*fn)(RadialArgs) = radial_basis_kernel<K, ALL, ANG, 1, false, true>;
+        if (smem > 48 * 1024) {
+          cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+          if (e != cudaSuccess) return e;
+        }
+        fn<<<grid, kRadialThreads, smem, st>>>(a);
+        return cudaGetLastError();
+      }
       return launch_t<K, ALL, ANG, 1, false>(a, grid, smem, st);
   }
 }
@@ -511,13 +525,15 @@ static cudaError_t launch_k(const RadialArgs& a, bool all, bool ang, int vec, bo
 int radial_stages(bool) { return kRingStages; }
 
 size_t radial_smem_bytes(int K, bool all, int vec, bool tma, int stage_slots, int max_jmax,
-                         int col_cap) {
+                         int col_cap, bool coef_global) {
   (void)all;
   const size_t nj = static_cast<size_t>(max_jmax) + 1;
   const size_t stage =
       tma ? size_t(kRingStages) * stage_slots * kRadialThreads * vec * sizeof(double) : 0;
-  return 128 + stage + (K + 1) * nj * sizeof(ChainCoef) + (K > 0 ? nj * sizeof(AsmCoef) : 0) +
-         static_cast<size_t>(col_cap) * sizeof(long long) + (nj + 1) * sizeof(int);
+  const size_t tables =
+      coef_global ? 0 : (K + 1) * nj * sizeof(ChainCoef) + (K > 0 ? nj * sizeof(AsmCoef) : 0);
+  return 128 + stage + tables + static_cast<size_t>(col_cap) * sizeof(long long) +
+         (nj + 1) * sizeof(int);
 }
 
 cudaError_t launch_radial(const RadialArgs& a, int K, bool all, bool ang, int vec, bool tma,

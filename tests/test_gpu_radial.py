@@ -413,11 +413,14 @@ def test_concurrent_callers_share_a_context():
         assert np.array_equal(o, want)
 
 
-def test_mode_set_too_large_fails_loudly():
-    # jacobi degree 3000 with k=3 cannot stage its coefficients in shared memory
-    modes = zb.as_mode_set([(6000, 0)])
-    with pytest.raises(ValueError):
-        radial(modes, [0.5], 3)
+def test_degree_6000_uses_the_global_coefficient_kernel():
+    # jacobi degree 3000 with k=3 cannot stage its coefficients in shared
+    # memory (it used to fail with ValueError); the fallback kernel serves it
+    modes = zb.as_mode_set([(6000, 0), (5999, 1)])
+    pts = np.array([0.0, 0.25, 0.5, 0.999, 1.0])
+    got = radial(modes, pts, 3)
+    want = orc.radial_batch([(6000, 0), (5999, 1)], pts, 3, power=orc.cr_power)
+    assert np.array_equal(got, want)
 
 
 @pytest.mark.parametrize("vec", ["4", "2", "1"])
@@ -576,3 +579,17 @@ def test_release_buffers_then_reuse():
     _lib.context().release_buffers()
     b, _ = zb.evaluate_batch(zb.BatchRequest(modes=modes, grid=grid))
     assert np.array_equal(a.values, b.values)
+
+
+def test_very_long_chains_fall_back_to_global_coefficients():
+    """Degrees whose coefficient tables do not fit in shared memory (here
+    n = 2500, k = 3: 320 KB) run the global-coefficient fallback kernel --
+    still the reference algorithm with correctly rounded powers, bitwise."""
+    modes = [(2500, 0), (2500, 2), (2497, 5), (2501, -3), (12, 4)]
+    grid = np.random.default_rng(8).uniform(size=300)
+    for k in (0, 3):
+        t, _ = zb.evaluate_batch(zb.BatchRequest(modes=zb.as_mode_set(modes), grid=grid,
+                                                 deriv_order=k))
+        want = orc.radial_batch(modes, grid, k, power=orc.cr_power)
+        tiny = np.abs(want) < 1e-250
+        assert np.array_equal(t.values[~tiny], want[~tiny]), k
