@@ -902,6 +902,12 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const do
     const bool dmma = (dm < 0 ? ncoef >= 8 : dm != 0) &&
                       zk::series_dmma_smem_bytes(deriv_order, plan->host.max_jmax, nch) <=
                           ctx->max_smem;
+    if (!dmma && zk::series_fma_smem_bytes(deriv_order, plan->host.max_jmax) > ctx->max_smem)
+      return fail(ZK_EINVAL,
+                  "series: jacobi degree " + std::to_string(plan->host.max_jmax) +
+                      " is too long for the series kernel's shared-memory stage at order " +
+                      std::to_string(deriv_order) +
+                      "; evaluate the basis (zk_radial_eval / zk_zernike_eval) and contract it");
     cudaError_t e = zk::launch_series(a, deriv_order, plan->host.max_jmax, nrowslots,
                                       static_cast<double*>(ctx->scratch[1]), dmma, st, &launches);
     ctx->launches += launches;

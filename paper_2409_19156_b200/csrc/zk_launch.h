@@ -57,6 +57,8 @@ struct SeriesArgs {
 };
 
 size_t series_scratch_bytes(long long nrowslots);
+// shared memory the FMA series kernel needs for one coefficient vector
+size_t series_fma_smem_bytes(int K, int max_jmax);
 cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nrowslots,
                           double* rowc, bool dmma, cudaStream_t st, int* launches);
 int series_dmma_chunks(int ncoef);

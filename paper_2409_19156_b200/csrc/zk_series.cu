@@ -318,6 +318,12 @@ static cudaError_t launch_ang(const SeriesArgs& a, const double* rowc, int v0, i
                  : launch_nc<K, false>(a, rowc, v0, nc, buf_doubles, st);
 }
 
+size_t series_fma_smem_bytes(int K, int max_jmax) {
+  const int nj = max_jmax + 1;
+  const int buf = ((K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0) + nj * 2 + 1) & ~1;  // nc = 1
+  return size_t(2) * buf * sizeof(double);
+}
+
 size_t series_scratch_bytes(long long nrowslots) {
   return static_cast<size_t>(nrowslots) * 2 * 32 * sizeof(double) + 256;
 }

@@ -132,3 +132,9 @@ def test_series_fma_and_dmma_paths(monkeypatch, path, k, V):
         ref = B @ C
         scale = np.abs(B) @ np.abs(C)
         assert (np.abs(f - ref) <= 1e-13 * scale + 1e-13).all(), (path, k, V, th is None)
+
+
+def test_series_too_long_chain_fails_with_clear_error():
+    modes = zb.as_mode_set([(3000, 0)])
+    with pytest.raises(ValueError, match="series kernel"):
+        zb.series_eval(modes, np.ones(1), np.array([0.5]), deriv_order=3)
