@@ -29,8 +29,13 @@ def run(seed: int, cases: int, verbose: bool = True) -> int:
     t_start = time.time()
     bad = 0
     for it in range(cases):
-        kind = rng.integers(0, 3)
-        if kind == 0:
+        kind = rng.integers(0, 7)
+        if kind == 6:  # very long chains: k = 3 runs the global-coefficient fallback
+            modes = []
+            for _ in range(int(rng.integers(1, 4))):
+                n = int(rng.integers(1800, 3001))
+                modes.append((n, -n + 2 * int(rng.integers(0, n + 1))))
+        elif kind == 0:
             modes = [(md.n, md.m) for md in zb.full_mode_set(int(rng.integers(0, 70)))]
         else:
             cnt = int(rng.integers(1, 400))
@@ -39,7 +44,7 @@ def run(seed: int, cases: int, verbose: bool = True) -> int:
             for _ in range(cnt):
                 n = int(rng.integers(0, nmax + 1))
                 modes.append((n, -n + 2 * int(rng.integers(0, n + 1))))
-            if kind == 2:  # duplicates and sign flips
+            if kind in (2, 4):  # duplicates and sign flips
                 modes += modes[: cnt // 3] + [(n, -m) for n, m in modes[: cnt // 4]]
         ms = zb.as_mode_set(modes)
         n = np.array([md.n for md in ms], np.int32)
@@ -77,16 +82,22 @@ def run(seed: int, cases: int, verbose: bool = True) -> int:
             if ang:
                 want = orc.basis_2d([(md.n, md.m) for md in ms], rho[idx], th[idx], kk)
                 got = ref_h[o][:, idx].T
-                scale = np.maximum(1.0, np.abs(want).max(axis=0))
-                ok = (np.abs(got - want) / scale <= 1e-12).all()
+                fin = np.isfinite(want)
+                same_special = np.array_equal(got[~fin], want[~fin], equal_nan=True)
+                scale = np.maximum(1.0, np.abs(np.where(fin, want, 0.0)).max(axis=0))
+                ok = same_special and (np.abs(np.where(fin, got - want, 0.0)) / scale
+                                       <= 1e-12).all()
             else:
                 want = orc.radial_batch([(md.n, md.m) for md in ms], rho[idx], kk, power=orc.cr_power)
                 got = ref_h[o][:, idx].T
                 tiny = np.abs(want) < 1e-250
-                ok = np.array_equal(got[~tiny], want[~tiny])
+                # (NaN where the reference algorithm itself overflows: a chain
+                # P_j^(a,b) beyond 1e308 times an underflowed rho^m -> 0 * inf)
+                ok = np.array_equal(got[~tiny], want[~tiny], equal_nan=True)
             if not ok:
                 bad += 1
-                print("ORACLE MISMATCH", it, M, P, k, all_orders, ang)
+                print("ORACLE MISMATCH", it, M, P, k, all_orders, ang, "| kind", int(kind),
+                      "| modes", modes[:3], "| rho", rho[idx][:3])
         # every other path
         ld = P + int(rng.integers(0, 3))
         ostride = ld * M + int(rng.integers(0, 5))
@@ -115,9 +126,14 @@ def run(seed: int, cases: int, verbose: bool = True) -> int:
                 res = dout.cpu().numpy()
             for o in range(NO):
                 blk = res[o * ostride:o * ostride + ld * M].reshape(M, ld)
-                if not np.array_equal(blk[:, :P], ref_h[o]) or not np.isnan(blk[:, P:]).all():
+                if (not np.array_equal(blk[:, :P], ref_h[o], equal_nan=True)
+                        or not np.isnan(blk[:, P:]).all()):
                     bad += 1
-                    print("PATH MISMATCH", it, flags, M, P, k, all_orders, ang, ld, ostride)
+                    print("PATH MISMATCH", it, flags, M, P, k, all_orders, ang, ld, ostride,
+                          "| value diffs", int((blk[:, :P] != ref_h[o]).sum()),
+                          "| pad writes", int((~np.isnan(blk[:, P:])).sum()),
+                          "| nan in ref", int(np.isnan(ref_h[o]).sum()), "| kind", int(kind),
+                          "| modes", modes[:3])
             if buf is not None:
                 del out, res
                 _lib.lib.zk_host_free(buf)
