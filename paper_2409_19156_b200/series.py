@@ -90,6 +90,23 @@ def gram(modes, rho, theta=None, y=None, device: int | None = None):
 # device-resident (torch) entry points
 # --------------------------------------------------------------------------
 
+def _device_f64(*named):
+    """Device entry points take CUDA float64 tensors on one device; anything
+    else would be reinterpreted bytes, so it is rejected up front."""
+    import torch
+    dev = None
+    for name, t in named:
+        if t is None:
+            continue
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
+            raise TypeError(f"{name} must be a CUDA float64 tensor, got "
+                            f"{type(t).__name__}{'' if not isinstance(t, torch.Tensor) else ' ' + str(t.dtype) + ' on ' + str(t.device)}")
+        if dev is None:
+            dev = t.device
+        elif t.device != dev:
+            raise ValueError(f"{name} is on {t.device}, expected {dev}")
+
+
 def _torch_ctx(tensor, device):
     import torch
     dev = tensor.device.index if device is None else device
@@ -106,6 +123,7 @@ def basis_device(plan_modes, rho, deriv_order: int = 0, theta=None, all_orders: 
     copy. Values are bitwise those of the numpy entry points. Zero-copy to
     other frameworks through DLPack (``torch.utils.dlpack.to_dlpack``)."""
     import torch
+    _device_f64(("rho", rho), ("theta", theta))
     ms, n, m = _modes(plan_modes)
     k = _check_order(deriv_order)
     M, P = len(ms), rho.numel()
@@ -132,6 +150,7 @@ def gram_device(plan_modes, rho, theta=None, y=None, G=None, Bty=None):
     """Accumulate G += B^T B, Bty += B^T y for CUDA tensors (float64) on the
     tensors' device, on torch's current stream. Returns (G, Bty)."""
     import torch
+    _device_f64(("rho", rho), ("theta", theta), ("y", y), ("G", G), ("Bty", Bty))
     ms, n, m = _modes(plan_modes)
     M = len(ms)
     dev = rho.device
@@ -156,6 +175,7 @@ def gram_device(plan_modes, rho, theta=None, y=None, G=None, Bty=None):
 def series_device(plan_modes, coef, rho, theta=None, deriv_order: int = 0):
     """f = B c for CUDA tensors (float64); coef (M,) or (M, V)."""
     import torch
+    _device_f64(("rho", rho), ("theta", theta), ("coef", coef))
     ms, n, m = _modes(plan_modes)
     k = _check_order(deriv_order)
     M = len(ms)

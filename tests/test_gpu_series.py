@@ -138,3 +138,15 @@ def test_series_too_long_chain_fails_with_clear_error():
     modes = zb.as_mode_set([(3000, 0)])
     with pytest.raises(ValueError, match="series kernel"):
         zb.series_eval(modes, np.ones(1), np.array([0.5]), deriv_order=3)
+
+
+def test_device_entry_points_reject_wrong_dtype_or_device():
+    import torch
+    modes = zb.full_mode_set(4)
+    rho32 = torch.rand(10, device="cuda", dtype=torch.float32)
+    with pytest.raises(TypeError):
+        zb.basis_device(modes, rho32)
+    with pytest.raises(TypeError):
+        zb.series_device(modes, torch.ones(len(modes), dtype=torch.float64), torch.rand(10, dtype=torch.float64))
+    with pytest.raises(TypeError):
+        zb.gram_device(modes, rho32.double().cpu())
