@@ -18,6 +18,8 @@
 
 namespace zk {
 
+constexpr int kDirectTab = 48;  // rho powers tabulated per point (local memory)
+
 __global__ void __launch_bounds__(128)
 direct_kernel(const double* __restrict__ rho, long long P, const double* __restrict__ coef,
               const int32_t* __restrict__ term_ptr, const int32_t* __restrict__ low_exp,
@@ -26,13 +28,25 @@ direct_kernel(const double* __restrict__ rho, long long P, const double* __restr
   if (p >= P) return;
   const double r = rho[p];
   const double u = __dmul_rn(r, r);
+  // rho^e for e < kDirectTab, once per point (double-double chain, rounded once
+  // per entry) instead of one exponentiation per column (4.4 -> 2.9 ms at
+  // n <= 40 x 1e6 points; a thread-strided shared-memory table measured slower)
+  double ptab[kDirectTab];
+  {
+    dd acc{1.0, 0.0};
+    for (int e = 0; e < kDirectTab; ++e) {
+      ptab[e] = acc.hi;
+      acc = dd_mul_d(acc, r);
+    }
+  }
   for (long long c = 0; c < M; ++c) {
     const int t0 = __ldg(term_ptr + c), t1 = __ldg(term_ptr + c + 1);
     double v = 0.0;  // zero polynomial (derivative of a low-degree mode)
     if (t1 > t0) {
       double acc = __ldg(coef + t0);
       for (int t = t0 + 1; t < t1; ++t) acc = __dadd_rn(__dmul_rn(acc, u), __ldg(coef + t));
-      v = __dmul_rn(acc, dd_pow(r, __ldg(low_exp + c)).hi);
+      const int le = __ldg(low_exp + c);
+      v = __dmul_rn(acc, le < kDirectTab ? ptab[le] : dd_pow(r, le).hi);
     }
     out[c * ld + p] = v;
   }
