@@ -87,6 +87,14 @@ int zk_ctx_synchronize(zk_ctx* ctx);
 int zk_ctx_release_buffers(zk_ctx* ctx);
 /* Number of kernels this ctx launched since creation (bench accounting). */
 int zk_ctx_launch_count(const zk_ctx* ctx, int64_t* count);
+/* Page-lock / release a caller-owned host range (cudaHostRegister, portable
+ * to every device) so results written into it cross PCIe at full DMA rate
+ * with no host-side bounce copy. The numpy API registers its recycled result
+ * buffers with this (hostpool.py); the range must stay allocated until
+ * zk_host_unregister. No reference counterpart: a host-memory service of the
+ * boundary, like zk_ctx_release_buffers. */
+int zk_host_register(void* ptr, size_t bytes);
+int zk_host_unregister(void* ptr);
 
 /* ---- mode planning (host-only; usable without a GPU) -------------------
  * Unique (n,|m|) keys in first-appearance order and the column -> key

@@ -52,6 +52,8 @@ SIGNATURES = {
     "zk_ctx_synchronize": (c_int, [c_void_p]),
     "zk_ctx_release_buffers": (c_int, [c_void_p]),
     "zk_ctx_launch_count": (c_int, [c_void_p, _i64p]),
+    "zk_host_register": (c_int, [c_void_p, ctypes.c_size_t]),
+    "zk_host_unregister": (c_int, [c_void_p]),
     "zk_plan_describe": (c_int, [_i32p, _i32p, c_int64, _i32p, _i32p, _i32p, _i64p]),
     "zk_step_counters": (c_int, [_i32p, _i32p, c_int64, c_int, c_int, _i64p, _i64p]),
     "zk_plan_create": (c_int, [c_void_p, _i32p, _i32p, c_int64, c_int, POINTER(c_void_p)]),

@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib
 from .evaluate import MAX_DERIV_ORDER, basis_matrix, parallel_devices
-from .modes import DedupPlan, ModeSet, as_mode_set, mode_arrays
+from .modes import DedupPlan, ModeSet, as_mode_set, mode_arrays, mode_set_entry
 from .tables import EvalMatrix, radial_grid
 
 STRATEGIES = ("cached", "independent")  # zk/batch.py:28
@@ -55,9 +55,13 @@ class BatchRequest:
 
 
 def _counter(modes, k: int, shared: bool) -> StepCounter:
-    n, m = mode_arrays(modes)
-    steps, chains = _lib.step_counters(n, m, k, shared)
-    return StepCounter(recursion_steps=steps, chain_count=chains)
+    _, n, m, memo = mode_set_entry(modes)
+    key = ("counter", int(k), bool(shared))
+    hit = memo.get(key)
+    if hit is None:
+        steps, chains = _lib.step_counters(n, m, k, shared)
+        hit = memo[key] = StepCounter(recursion_steps=steps, chain_count=chains)
+    return hit
 
 
 def _plan_arrays(plan: DedupPlan) -> tuple[np.ndarray, np.ndarray]:

@@ -435,6 +435,46 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
     return ZK_OK;
   }
 
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+
+  // Small dense results (the reference CLI's bench sizes): one launch into a
+  // dense device image of the result and ONE contiguous D2H straight into it.
+  // Below a few MB (pageable destination, ZK_SMALL_MB) or a few tens of MB
+  // (page-locked, ZK_SMALL_PINNED_MB: the DMA runs at full PCIe rate) the
+  // pipeline's fixed costs -- per-column 2-D copies, host-pool wake-ups for the
+  // bounce scatter and the repeated-column fill -- dominate: 100 points x 5,151
+  // modes 2.3 -> 0.3 ms per call, 1,000 points x 5,151 modes 2.8 -> ~1 ms.
+  const size_t out_bytes = size_t(NO) * size_t(P) * size_t(M) * 8;
+  const size_t small_mb = size_t(std::max(
+      0, pinned ? env_int("ZK_SMALL_PINNED_MB", 64) : env_int("ZK_SMALL_MB", 8)));
+  if (ld == P && (!all || ostride == P * M) && out_bytes <= (small_mb << 20)) {
+    const size_t in_bytes = align_up(size_t(P) * 8, 256);
+    const size_t img = align_up(out_bytes, 256);
+    int rc = ensure_scratch(ctx, 0, img + in_bytes * nin);
+    if (rc) return rc;
+    double* dbasis = static_cast<double*>(ctx->scratch[0]);
+    const double* r_in = rho;
+    const double* t_in = ang ? theta : nullptr;
+    if (host_in) {
+      double* din = dbasis + img / 8;
+      ZK_CUDA(cudaMemcpyAsync(din, rho, size_t(P) * 8, cudaMemcpyHostToDevice, ctx->stream));
+      r_in = din;
+      if (ang) {
+        ZK_CUDA(cudaMemcpyAsync(din + in_bytes / 8, theta, size_t(P) * 8,
+                                cudaMemcpyHostToDevice, ctx->stream));
+        t_in = din + in_bytes / 8;
+      }
+    }
+    rc = launch_device(ctx, plan, r_in, t_in, P, k, all, dbasis, P, P * M, scalar, ctx->stream);
+    if (rc) return rc;
+    ZK_CUDA(cudaMemcpyAsync(out, dbasis, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+    return ZK_OK;
+  }
+
   // host output: chunk the points, double-buffered compute -> D2H pipeline on
   // two streams so chunk c's copy overlaps chunk c+1's kernel.
   // Radial basis with repeated keys (every +-m pair of a full set): the chunk
@@ -442,10 +482,6 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
   // columns and the host fills the others from their key's first column.
   // Pageable destination (e.g. a fresh numpy array): D2H into pinned bounce
   // buffers, then the host pool scatters each chunk into place in parallel.
-  cudaPointerAttributes pa{};
-  const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess &&
-                      pa.type == cudaMemoryTypeHost;
-  cudaGetLastError();
   const bool bounce = !pinned && env_int("ZK_BOUNCE", 1) != 0;
   zk_plan* mplan = const_cast<zk_plan*>(plan);
   const bool uniq = !ang && static_cast<int64_t>(plan->host.key_n.size()) < M &&
@@ -705,6 +741,26 @@ int zk_ctx_release_buffers(zk_ctx* ctx) {
     if (ctx->hbounce[s]) cudaFreeHost(ctx->hbounce[s]);
     ctx->hbounce[s] = nullptr;
     ctx->hbounce_bytes[s] = 0;
+  }
+  return ZK_OK;
+}
+
+int zk_host_register(void* ptr, size_t bytes) {
+  if (!ptr || bytes == 0) return fail(ZK_EINVAL, "null or empty host range");
+  cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_fail(e, "cudaHostRegister");
+  }
+  return ZK_OK;
+}
+
+int zk_host_unregister(void* ptr) {
+  if (!ptr) return fail(ZK_EINVAL, "null host pointer");
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_fail(e, "cudaHostUnregister");
   }
   return ZK_OK;
 }

@@ -39,6 +39,7 @@ _TARGETS = {
 def _wrappers(zk):
     from . import _lib
     from .evaluate import basis_matrix, parallel_devices
+    from .modes import mode_set_entry
 
     ref_eval = importlib.import_module(zk.__name__ + ".evaluate")
     ref_batch = importlib.import_module(zk.__name__ + ".batch")
@@ -47,10 +48,6 @@ def _wrappers(zk):
     orig = {name: getattr(ref_eval, name) for name in _TARGETS["evaluate"]}
     orig.update({name: getattr(ref_batch, name) for name in _TARGETS["batch"]})
 
-    def _arrays(modes):
-        n = np.fromiter((md.n for md in modes), np.int32, len(modes))
-        m = np.fromiter((md.m for md in modes), np.int32, len(modes))
-        return n, m
 
     def radial_jacobi(n, m_abs, grid, deriv_order=0):
         # validation exactly as zk/evaluate.py:173-176, with the reference's types
@@ -80,13 +77,19 @@ def _wrappers(zk):
     def _run(request, shared, parallel):
         # parallel=True: the reference's thread pool (zk/batch.py:136-141)
         # becomes point shards over every visible GPU; bitwise the same values
-        n, m = _arrays(request.modes)
+        # mode arrays and counters memoised per mode-set tuple (modes.py)
+        _, n, m, memo = mode_set_entry(request.modes)
         values = basis_matrix(n, m, request.grid, request.deriv_order,
                               devices=parallel_devices() if parallel else None)
-        steps, chains = _lib.step_counters(n, m, request.deriv_order, shared)
+        key = ("ref_counter", int(request.deriv_order), bool(shared))
+        counter = memo.get(key)
+        if counter is None:
+            steps, chains = _lib.step_counters(n, m, request.deriv_order, shared)
+            counter = memo[key] = ref_batch.StepCounter(recursion_steps=steps,
+                                                        chain_count=chains)
         table = ref_tables.EvalMatrix(values=values, modes=request.modes,
                                       deriv_order=request.deriv_order)
-        return table, ref_batch.StepCounter(recursion_steps=steps, chain_count=chains)
+        return table, counter
 
     def batch_cached(request, parallel=False):
         if request.strategy != "cached":

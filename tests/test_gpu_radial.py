@@ -593,3 +593,76 @@ def test_very_long_chains_fall_back_to_global_coefficients():
         want = orc.radial_batch(modes, grid, k, power=orc.cr_power)
         tiny = np.abs(want) < 1e-250
         assert np.array_equal(t.values[~tiny], want[~tiny]), k
+
+
+@pytest.mark.parametrize("ang", [False, True])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_small_dense_host_output_equals_device_output(monkeypatch, ang, pinned):
+    """Host outputs up to ZK_SMALL_MB take the one-launch / one-D2H path
+    (zk_capi.cu eval_common); bitwise the device result and the chunked
+    pipeline's, for odd point counts, all orders, the 2-D basis and
+    pinned / pageable destinations; ld > P keeps the pipeline."""
+    rng = np.random.default_rng(5)
+    modes = zb.full_mode_set(30)
+    M, k = len(modes), 2
+    ctx, plan = _plan(modes)
+    for P, extra in ((1, 0), (37, 0), (1001, 0), (1001, 3)):
+        ld = P + extra
+        ostride = ld * M
+        grid = rng.uniform(size=P)
+        theta = rng.uniform(0, 2 * np.pi, size=P)
+        d_rho = torch.tensor(grid, device="cuda")
+        d_th = torch.tensor(theta, device="cuda")
+        dev = torch.empty((k + 1) * ostride, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+
+        def call(rho, th, out, flags):
+            if ang:
+                return _lib.lib.zk_zernike_eval(ctx.handle, plan.handle, rho, th, P, k, 1, out,
+                                                ld, ostride, flags)
+            return _lib.lib.zk_radial_eval(ctx.handle, plan.handle, rho, P, k, 1, out, ld,
+                                           ostride, flags)
+
+        _lib.check(call(d_rho.data_ptr(), d_th.data_ptr(), dev.data_ptr(), 0), "device")
+        ref = dev.cpu().numpy()
+        flags = _lib.ZK_HOST_INPUT | _lib.ZK_HOST_OUTPUT
+        for small in ("8", "0"):
+            monkeypatch.setenv("ZK_SMALL_MB", small)
+            if pinned:
+                host = torch.full(((k + 1) * ostride,), np.nan, dtype=torch.float64,
+                                  pin_memory=True).numpy()
+            else:
+                host = np.full((k + 1) * ostride, np.nan)
+            _lib.check(call(grid.ctypes.data, theta.ctypes.data, host.ctypes.data, flags),
+                       "host")
+            for o in range(k + 1):
+                a = ref[o * ostride:(o + 1) * ostride].reshape(M, ld)[:, :P]
+                b = host[o * ostride:(o + 1) * ostride].reshape(M, ld)
+                assert np.array_equal(a, b[:, :P]), (P, extra, small, o)
+                assert np.isnan(b[:, P:]).all()
+
+
+def test_recycled_result_buffers_are_page_locked(monkeypatch):
+    """hostpool: a reused result buffer is registered with zk_host_register,
+    results written into it are bitwise the unpinned ones, and eviction /
+    clear() unregister it."""
+    import gc
+
+    from paper_2409_19156_b200 import hostpool
+
+    pool = hostpool.ResultPool(1 << 30)
+    monkeypatch.setattr(hostpool, "POOL", pool)
+    req = zb.BatchRequest(modes=zb.full_mode_set(60), grid=zb.linear_radial_grid(3001))
+    first = zb.evaluate_batch(req)[0].values  # fresh buffer (pageable, bounce path)
+    want = first.copy()
+    del first
+    gc.collect()
+    t = zb.evaluate_batch(req)[0]  # recycled -> page-locked -> direct DMA path
+    assert [v for v in pool.pinned.values() if v] == [t.values.ctypes.data]
+    assert np.array_equal(t.values, want)
+    again = zb.evaluate_batch(req)[0]  # a second buffer (t still alive): fresh
+    assert np.array_equal(again.values, want)
+    del t, again
+    gc.collect()
+    pool.clear()
+    assert not pool.pinned

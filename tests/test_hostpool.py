@@ -37,3 +37,41 @@ def test_cap_evicts_and_small_arrays_bypass():
     assert small.base is None
     off = hostpool.ResultPool(0)
     assert off.take(3_000_000).base is None
+
+
+def test_mode_arrays_memoised_per_mode_set():
+    """modes.mode_set_entry: one (n, m) walk per mode-set tuple, read-only
+    arrays, identity-keyed (an equal but distinct tuple gets its own entry)."""
+    from paper_2409_19156_b200 import modes as zm
+
+    ms = zm.full_mode_set(12)
+    n1, m1 = zm.mode_arrays(ms)
+    n2, m2 = zm.mode_arrays(ms)
+    assert n1 is n2 and m1 is m2
+    assert not n1.flags.writeable and not m1.flags.writeable
+    assert n1.tolist() == [md.n for md in ms] and m1.tolist() == [md.m for md in ms]
+    twin = tuple(list(ms))
+    assert twin is not ms and zm.mode_arrays(twin)[0] is not n1
+    lst = list(ms)  # non-tuples are not memoised
+    assert zm.mode_arrays(lst)[0] is not zm.mode_arrays(lst)[0]
+
+
+def test_pinning_failure_is_silent_without_a_device():
+    """A recycled buffer that cannot be page-locked (no GPU here) is used
+    unpinned, and is not retried."""
+    import torch
+
+    if torch.cuda.is_available():
+        import pytest
+        pytest.skip("CPU-only check")
+    pool = hostpool.ResultPool(1 << 30)
+    a = pool.take(200_000)
+    del a
+    gc.collect()
+    b = pool.take(200_000)
+    assert list(pool.pinned.values()) == [0]
+    b[:] = 2.0
+    del b
+    gc.collect()
+    pool.clear()
+    assert not pool.pinned
