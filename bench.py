@@ -7,9 +7,10 @@ and rank r evaluates its contiguous shard (weak scaling, no communication).
 
 Arms
   default            libzk_b200 (CUDA, sm_100a) through the C ABI.
-  --impl reference   the reference's own CPU algorithm (oracle/zk_oracle.py, a
-                     bitwise-faithful numpy port of zernkit.batch_cached with its
-                     thread pool) on the host cores, bounded sample per step.
+  --impl reference   the reference's own CPU path, zernkit.batch_cached with its
+                     thread pool, on the host cores, bounded sample per step: the
+                     unmodified package from baseline/_ref when it is installed
+                     there, else its bitwise-faithful numpy port (oracle/zk_oracle.py).
 
 Timing: W warm-up steps, then K steps bracketed by barrier + synchronize,
 CUDA events on the launching stream, max over ranks. The 4.12 GB output is
@@ -127,23 +128,60 @@ def dist_setup():
     return world, rank, local
 
 
+def real_reference():
+    """The unmodified reference package when it was installed into the
+    git-ignored baseline/_ref (`pip install --target baseline/_ref`, DESIGN
+    §7), else None (ZK_REF_ARM=port forces the numpy port)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.environ.get("ZK_REF_ARM", "auto") == "port" or not os.path.isdir(
+            os.path.join(ref, "zernkit")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        import zernkit
+    except Exception:
+        return None
+    finally:
+        sys.path.remove(ref)
+    return zernkit
+
+
 def cpu_reference_rate(sample_points: int, reps: int, warmup: int = 1):
-    """The reference algorithm (numpy port, thread pool over alpha groups,
-    zk/batch.py:136-138) on a bounded sample of the config-2 grid."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import zk_oracle as orc  # checker / CPU baseline only
-    modes = orc.full_modes(N_RES)
-    full = orc.Workload(N_RES, P_PER_GPU).grid()
-    pts = full[:: max(1, full.size // sample_points)][:sample_points]
+    """The reference's CPU path -- zernkit.batch_cached(parallel=True), its
+    thread pool over alpha groups (zk/batch.py:104-142) -- on a bounded
+    sample of the config-2 grid: the unmodified reference from baseline/_ref
+    when present ("reference"), else the bitwise-faithful numpy port
+    (oracle/zk_oracle.py, "port"). Returns (rate, s/step, points, modes, kind)."""
+    zk = real_reference()
+    if zk is not None:
+        modes = zk.full_mode_set(N_RES)
+        full = zk.linear_radial_grid(P_PER_GPU)
+        pts = full[:: max(1, full.size // sample_points)][:sample_points]
+        request = zk.BatchRequest(modes=modes, grid=pts)
+        run, kind = (lambda: zk.batch_cached(request, parallel=True)), "reference"
+    else:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import zk_oracle as orc  # checker / CPU baseline only
+        modes = orc.full_modes(N_RES)
+        full = orc.Workload(N_RES, P_PER_GPU).grid()
+        pts = full[:: max(1, full.size // sample_points)][:sample_points]
+        run, kind = (lambda: orc.radial_batch(modes, pts, 0, parallel=True)), "port"
     times = []
     for i in range(warmup + reps):
         t0 = time.perf_counter()
-        orc.radial_batch(modes, pts, 0, parallel=True)
+        run()
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
     t = statistics.median(times)
-    return pts.size * len(modes) / t, t, pts.size, len(modes)
+    return pts.size * len(modes) / t, t, pts.size, len(modes), kind
+
+
+def ref_label(kind: str) -> str:
+    if kind == "reference":
+        return ("the unmodified reference, zernkit 0.1.0 batch_cached(parallel=True) "
+                "from baseline/_ref")
+    return "numpy port of zernkit.batch_cached(parallel=True) (oracle/zk_oracle.py)"
 
 
 def host_cores():
@@ -161,8 +199,8 @@ def run_reference(args, world, rank):
     # per step beyond that (small samples understate the CPU rate: numpy's
     # per-call overhead is amortised over fewer points)
     sample = int(min(args.ref_sample, max(1000, args.ref_sample * 200 // max(1, args.steps))))
-    rate, t, npts, M = cpu_reference_rate(sample, reps=max(1, args.steps),
-                                          warmup=max(0, min(args.warmup, 1)))
+    rate, t, npts, M, kind = cpu_reference_rate(sample, reps=max(1, args.steps),
+                                                warmup=max(0, min(args.warmup, 1)))
     cores = host_cores()
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "impl": "reference",
@@ -172,9 +210,9 @@ def run_reference(args, world, rank):
         "config": {"workload": f"full mode set n<={N_RES} ({M} modes) x {P_PER_GPU} radial points "
                                f"per GPU, k=0 (sampled: {npts} points per step)",
                    "parallelism": "host threads"},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": f"{npts} of the {P_PER_GPU} config-2 grid points x {M} modes "
-                                   f"per step; numpy port of zernkit.batch_cached(parallel=True), "
+                                   f"per step; {ref_label(kind)}, "
                                    f"ThreadPoolExecutor default workers min(32, cpu+4)"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -329,10 +367,10 @@ def run_gpu(args, world, rank, local):
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        rate, t, npts, _ = cpu_reference_rate(args.ref_sample, reps=3)
-        cpu = {"value": rate, "unit": UNIT, "cores": host_cores(), "kind": "port",
+        rate, t, npts, _, kind = cpu_reference_rate(args.ref_sample, reps=3)
+        cpu = {"value": rate, "unit": UNIT, "cores": host_cores(), "kind": kind,
                "sample": f"{npts} of {P} config-2 points x {M} modes, median of 3 after 1 warm-up; "
-                         "numpy port of zernkit.batch_cached(parallel=True)"}
+                         f"{ref_label(kind)}"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

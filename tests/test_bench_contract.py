@@ -27,7 +27,7 @@ def test_reference_arm_json_line():
     d = _run(["--impl", "reference", "--steps", "2", "--warmup", "1", "--ref-sample", "300"])
     assert BASE_KEYS <= set(d)
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 == d["e2e"]["d2h_bytes_per_step"]
     assert "workload" in d["config"]
