@@ -41,6 +41,7 @@ METRIC = "fp64 Zernike radial evals/s (points x modes)"
 UNIT = "evals/s"
 N_RES = 100
 P_PER_GPU = 100_000
+STORE_CEILING_GBS = 6924.9  # tools/hbm_write_probe.cu, 32-B stores, 16 CTAs/SM
 
 
 def load_peaks():
@@ -385,7 +386,12 @@ def run_gpu(args, world, rank, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy r+w)",
-                     "alg_bytes_per_launch": alg_bytes},
+                     "alg_bytes_per_launch": alg_bytes,
+                     # the output is write-only: the copy peak (r+w) understates a
+                     # pure-store kernel's ceiling; best incompressible streaming-store
+                     # kernel measured in round 1 (profiles/r01_hbm_write_probe.txt)
+                     "store_ceiling_gbs": STORE_CEILING_GBS,
+                     "frac_of_store_ceiling": achieved / STORE_CEILING_GBS},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
