@@ -423,6 +423,33 @@ def test_degree_6000_uses_the_global_coefficient_kernel():
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_subnormal_rho_powers(k):
+    """Where rho^(|m|+k) < 2^-916 the double-double power window's error terms
+    underflow, so the bitwise claim (the reference algorithm with correctly
+    rounded powers) covers only entries whose window stays above that; below,
+    the power is within a few subnormal ulps -- inside the parity tolerance,
+    and numpy's own pow (the reference) is not correctly rounded there either.
+    High-degree cases (values ~1e-200 from subnormal powers times huge chains)
+    found by tools/fuzz_paths.py seed 777; DESIGN.md section 3."""
+    from fractions import Fraction
+    pairs_ = [(2008, -1876), (2281, -483), (2031, 1071), (1928, 1778), (2515, -703),
+              (400, 380), (600, 560), (40, 12)]
+    modes = zb.as_mode_set(pairs_)
+    pts = np.array([0.6810649396839922, 0.6629706704580528, 0.50270979, 0.82940846,
+                    0.02, 0.15, 0.3, 1e-160, 0.0])
+    got = radial(modes, pts, k)
+    want = orc.radial_batch([(md.n, md.m) for md in modes], pts, k, power=orc.cr_power)
+    exact = np.array([[float(Fraction(float(r)) ** (abs(md.m) + k)) >= 2.0 ** -916
+                       for md in modes] for r in pts])
+    fin = np.isfinite(want)
+    assert (exact & fin).sum() > 20 and (~exact & fin & (np.abs(want) > 1e-250)).sum() > 0
+    assert np.array_equal(got[exact], want[exact], equal_nan=True)
+    assert np.array_equal(np.isfinite(got), fin)
+    err = np.abs(np.where(fin, got - want, 0.0))
+    assert (err <= 1e-13 + 1e-12 * np.abs(np.where(fin, want, 0.0))).all()
+
+
 @pytest.mark.parametrize("vec", ["4", "2", "1"])
 def test_store_paths_agree_bitwise(monkeypatch, vec):
     """Every store path (32/16/8-byte direct stores; the TMA bulk-store ring
