@@ -25,6 +25,8 @@
  *                                          reference: tests/test_acceptance.py:150-172)
  *   zk_direct_eval / zk_ztt_eval        <- zk/evaluate.py:189-247 float baselines
  *   zk_radial_eval_dd                   <- zk/exact.py:129-169 oracle_table (accuracy study)
+ *   zk_gram_allreduce / zk_comm_*       <- new (K5, NCCL sum of the partial normal
+ *                                          equations across GPUs)
  *
  * Conventions
  *   - Every function returns int: ZK_OK (0) or a negative ZK_E* code; the
@@ -158,6 +160,35 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho,
 int zk_gram_accumulate(zk_ctx* ctx, const zk_plan* plan, const double* rho,
                        const double* theta, int64_t P, const double* y,
                        double* G, double* Bty, uint32_t flags);
+
+/* ---- K5: the cross-GPU sum of the normal equations ----------
+ * Replaces nothing in the reference (single-process numpy, no collectives;
+ * its thread pool zk/batch.py:136-141 becomes point sharding over GPUs). The
+ * partial G_g (M x M, symmetric) and Bty_g of every GPU are summed with ONE
+ * ncclAllReduce(sum, fp64) of the packed upper triangle plus Bty --
+ * M(M+1)/2 + M doubles (C5: 14.3 MB + 15 KB), half of the full G -- then
+ * unpacked into the full symmetric G in place. NCCL is loaded at first use
+ * (dlopen libnccl.so.2); without it these calls fail with ZK_ENODEV.
+ * All buffers are device buffers; ZK_ASYNC skips the final synchronize. */
+int64_t zk_gram_packed_count(int64_t M);  /* M(M+1)/2 + M */
+int zk_gram_pack(zk_ctx* ctx, const double* G, const double* Bty, int64_t M, double* packed,
+                 uint32_t flags);  /* Bty may be NULL (its slots are zeroed) */
+int zk_gram_unpack(zk_ctx* ctx, const double* packed, int64_t M, double* G, double* Bty,
+                   uint32_t flags);  /* Bty may be NULL */
+int zk_nccl_version(int* version);
+/* One process driving n GPUs: ctxs[i] on distinct devices, G[i]/Bty[i] on
+ * ctxs[i]'s device (Bty may be NULL). ncclCommInitAll over the devices
+ * (cached per device list), grouped allreduce on each ctx's stream. */
+int zk_gram_allreduce(zk_ctx** ctxs, int n, double** G, double** Bty, int64_t M,
+                      uint32_t flags);
+/* One process per GPU: rank 0 makes a 128-byte id (zk_comm_unique_id), the
+ * launcher broadcasts it, every rank calls zk_comm_create on its ctx. */
+typedef struct zk_comm zk_comm;
+int zk_comm_unique_id(void* id_out /* 128 bytes */);
+int zk_comm_create(zk_ctx* ctx, const void* id, int nranks, int rank, zk_comm** out);
+int zk_comm_info(const zk_comm* comm, int* nranks, int* rank);
+int zk_comm_destroy(zk_comm* comm);
+int zk_gram_allreduce_comm(zk_comm* comm, double* G, double* Bty, int64_t M, uint32_t flags);
 
 /* ---- jacobi_chain export ------------------------------------------------
  * Rows P_0..P_{j_max} of the Jacobi chain (alpha, beta >= 0) at x[N]:

@@ -53,7 +53,9 @@ from .series import (
     gram,
     basis_device,
     gram_device,
+    pack_normal_equations,
     series_device,
+    unpack_normal_equations,
     series_eval,
     solve_normal,
 )
@@ -79,6 +81,7 @@ __all__ = [
     "linear_radial_grid", "make_mode", "radial_at_zero", "radial_grid", "radial_jacobi",
     "rational_radial_grid", "zernike_basis", "zernike_eval", "zernike_radial",
     "series_eval", "series_device", "basis_device", "gram", "gram_device", "fit", "fit_sharded",
-    "solve_normal", "allreduce_normal_equations", "shard_range", "radial_basis_shard",
+    "solve_normal", "allreduce_normal_equations", "pack_normal_equations",
+    "unpack_normal_equations", "shard_range", "radial_basis_shard",
     "radial_direct", "radial_direct_table", "radial_ztt", "radial_ztt_table",
 ]

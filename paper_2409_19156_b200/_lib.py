@@ -29,6 +29,8 @@ ZK_HOST_OUTPUT = 2
 ZK_ASYNC = 4
 ZK_STORE_SCALAR = 8
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -75,6 +77,17 @@ SIGNATURES = {
                             c_void_p, c_int64, c_uint32]),
     "zk_radial_eval_dd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int,
                                   c_void_p, c_int64, c_uint32]),
+    "zk_gram_packed_count": (c_int64, [c_int64]),
+    "zk_gram_pack": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_uint32]),
+    "zk_gram_unpack": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_uint32]),
+    "zk_nccl_version": (c_int, [POINTER(c_int)]),
+    "zk_gram_allreduce": (c_int, [POINTER(c_void_p), c_int, POINTER(c_void_p), POINTER(c_void_p),
+                                  c_int64, c_uint32]),
+    "zk_comm_unique_id": (c_int, [c_void_p]),
+    "zk_comm_create": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_void_p)]),
+    "zk_comm_info": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int)]),
+    "zk_comm_destroy": (c_int, [c_void_p]),
+    "zk_gram_allreduce_comm": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_uint32]),
     "zk_host_alloc": (c_int, [c_int64, POINTER(c_void_p)]),
     "zk_host_free": (c_int, [c_void_p]),
 }
@@ -155,7 +168,18 @@ class Context:
         check(lib.zk_ctx_release_buffers(self.handle), "zk_ctx_release_buffers")
 
     def set_stream(self, stream_ptr: int | None) -> None:
+        """Launch on the caller's cudaStream_t; None / 0 = the ctx's own stream."""
         check(lib.zk_ctx_set_stream(self.handle, c_void_p(stream_ptr or 0)), "zk_ctx_set_stream")
+
+    def use_torch_stream(self, device: int | None = None) -> None:
+        """Launch on torch's current stream of this ctx's device. torch's
+        default stream is the legacy default stream (handle 0), which the C
+        ABI would read as "the ctx's own (non-blocking) stream"; it is passed
+        as cudaStreamLegacy instead, so the kernels stay ordered with torch's
+        work either way."""
+        import torch
+        h = torch.cuda.current_stream(self.device if device is None else device).cuda_stream
+        self.set_stream(h if h else CUDA_STREAM_LEGACY)
 
     def synchronize(self) -> None:
         check(lib.zk_ctx_synchronize(self.handle), "zk_ctx_synchronize")
@@ -191,6 +215,46 @@ class Plan:
         if h is not None and lib is not None:
             lib.zk_plan_destroy(h)
             self.handle = None
+
+
+class Comm:
+    """zk_comm: one NCCL rank of the K5 normal-equation allreduce, bound to a
+    Context (one process per GPU). ``unique_id()`` on rank 0, shared by the
+    launcher (e.g. a torch.distributed broadcast), then ``Comm(ctx, id, N, r)``
+    on every rank."""
+
+    def __init__(self, ctx: Context, uid: bytes, nranks: int, rank: int):
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self.ctx = ctx
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        h = c_void_p()
+        check(lib.zk_comm_create(ctx.handle, buf, int(nranks), int(rank), ctypes.byref(h)),
+              "zk_comm_create")
+        self.handle = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(lib.zk_comm_unique_id(buf), "zk_comm_unique_id")
+        return buf.raw
+
+    def info(self) -> tuple[int, int]:
+        n, r = c_int(0), c_int(0)
+        check(lib.zk_comm_info(self.handle, ctypes.byref(n), ctypes.byref(r)), "zk_comm_info")
+        return n.value, r.value
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and lib is not None:
+            lib.zk_comm_destroy(h)
+            self.handle = None
+
+
+def nccl_version() -> int:
+    v = c_int(0)
+    check(lib.zk_nccl_version(ctypes.byref(v)), "zk_nccl_version")
+    return v.value
 
 
 _ctx_lock = threading.Lock()

@@ -20,8 +20,9 @@
 #include "../../include/zk_b200.h"
 #include "zk_internal.h"
 #include "zk_launch.h"
+#include "zk_ctx.h"
 
-namespace {
+namespace zk {
 
 thread_local std::string g_err;
 
@@ -34,17 +35,14 @@ int cuda_fail(cudaError_t e, const char* what) {
   return fail(ZK_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-#define ZK_CUDA(call)                                   \
-  do {                                                  \
-    cudaError_t e_ = (call);                            \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
-  } while (0)
+}  // namespace zk
 
-size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+using zk::align_up;
+using zk::cuda_fail;
+using zk::fail;
+using zk::g_err;
 
-}  // namespace
-
-namespace {
+namespace zk {
 
 // Persistent host worker pool for the pageable-output scatter (a fresh numpy
 // array is pageable: the D2H lands in pinned bounce buffers and these threads
@@ -111,59 +109,9 @@ class HostPool {
   bool stop_ = false;
 };
 
-}  // namespace
+}  // namespace zk
 
-struct zk_ctx {
-  int device = 0;
-  int sm_count = 148;
-  size_t max_smem = 48 * 1024;
-  cudaStream_t own = nullptr;     // default launch stream
-  cudaStream_t stream = nullptr;  // current launch stream (own or caller's)
-  cudaStream_t pipe[2] = {nullptr, nullptr};
-  cudaEvent_t ev_start = nullptr;
-  // device scratch for host-pointer calls: per pipeline slot
-  void* scratch[2] = {nullptr, nullptr};
-  size_t scratch_bytes[2] = {0, 0};
-  // pinned bounce buffers + events for pageable host outputs, per slot
-  void* hbounce[2] = {nullptr, nullptr};
-  size_t hbounce_bytes[2] = {0, 0};
-  cudaEvent_t ev_done[2] = {nullptr, nullptr};
-  HostPool* pool = nullptr;
-  std::vector<cudaEvent_t> chunk_ev;  // per-chunk D2H completion (unique-column path)
-  int64_t launches = 0;
-  std::mutex mu;  // one call at a time per ctx
-};
-
-struct zk_plan {
-  zk_ctx* ctx = nullptr;
-  zk::HostPlan host;
-  void* dmem = nullptr;
-  const zk::GroupRec* groups = nullptr;
-  const int32_t* order = nullptr;
-  const int32_t* rowptr = nullptr;
-  const int32_t* cols = nullptr;
-  const zk::ChainCoef* coef = nullptr;
-  const zk::AsmCoef* asmc = nullptr;
-  // Unique-column views for host outputs of the radial basis (built on first
-  // use): the kernel writes the "sent" columns -- one per unique (n, |m|)
-  // key, its first column, plus optionally a share of the repeated columns --
-  // and only those cross PCIe; every other column is a host copy of its key's
-  // first column. This is the reference's own unique -> scatter structure
-  // (zk/batch.py:97-101, zk/modes.py:108-125). (Sending a share of the
-  // repeated columns over PCIe as well, to offload the host fill, measured
-  // slower at every share: 5-30 % -> +1..+9 ms at config 2.)
-  struct Run {
-    int64_t s0, c0, len;  // sent columns s0.. land in output columns c0..
-  };
-  struct UView {
-    zk_plan* kplan = nullptr;                        // plan over the sent columns
-    std::vector<int64_t> slot;                       // output column -> sent slot to copy
-    std::vector<Run> runs;                           // contiguous sent-column runs
-    std::vector<std::pair<int64_t, int64_t>> fill;   // (output column, source column)
-    bool built = false;
-  };
-  UView uv;
-};
+using zk::HostPool;
 
 namespace {
 
@@ -681,6 +629,7 @@ int zk_ctx_create(int device, zk_ctx** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pipe[0], cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pipe[1], cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_switch, cudaEventDisableTiming);
   for (int s = 0; s < 2 && e == cudaSuccess; ++s)
     e = cudaEventCreateWithFlags(&ctx->ev_done[s], cudaEventDisableTiming | cudaEventBlockingSync);
   if (e != cudaSuccess) {
@@ -705,6 +654,8 @@ int zk_ctx_destroy(zk_ctx* ctx) {
     cudaStreamDestroy(ctx->own);
   }
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+  if (ctx->ev_switch) cudaEventDestroy(ctx->ev_switch);
+  if (ctx->comm_buf) cudaFree(ctx->comm_buf);
   for (int s = 0; s < 2; ++s) {
     if (ctx->ev_done[s]) cudaEventDestroy(ctx->ev_done[s]);
     if (ctx->hbounce[s]) cudaFreeHost(ctx->hbounce[s]);
@@ -717,7 +668,17 @@ int zk_ctx_destroy(zk_ctx* ctx) {
 
 int zk_ctx_set_stream(zk_ctx* ctx, void* stream) {
   if (!ctx) return fail(ZK_EINVAL, "null ctx");
-  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t next = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  if (next == ctx->stream) return ZK_OK;
+  // The ctx's scratch buffers (staging, Gram panel, series row sums, K5
+  // buffer) are ordered only by the launch stream: work queued on the new
+  // stream must not start before asynchronous (ZK_ASYNC) work that the old
+  // stream may still be running on the same scratch.
+  ZK_CUDA(cudaSetDevice(ctx->device));
+  ZK_CUDA(cudaEventRecord(ctx->ev_switch, ctx->stream));
+  ZK_CUDA(cudaStreamWaitEvent(next, ctx->ev_switch, 0));
+  ctx->stream = next;
   return ZK_OK;
 }
 
@@ -742,6 +703,9 @@ int zk_ctx_release_buffers(zk_ctx* ctx) {
     ctx->hbounce[s] = nullptr;
     ctx->hbounce_bytes[s] = 0;
   }
+  if (ctx->comm_buf) cudaFree(ctx->comm_buf);
+  ctx->comm_buf = nullptr;
+  ctx->comm_bytes = 0;
   return ZK_OK;
 }
 

@@ -28,7 +28,8 @@ def dist_env() -> tuple[int, int, int]:
 def radial_basis_shard(modes, rho_global, world: int, rank: int, deriv_order: int = 0,
                        device: int | None = None):
     """This rank's (P_r, M) block of the global basis, as a CUDA tensor
-    (column-major) on ``device`` (default: the local rank's GPU)."""
+    (column-major) on ``device`` (default: LOCAL_RANK's GPU under torchrun, else
+    torch's current device)."""
     import torch
 
     from . import _lib
@@ -38,13 +39,15 @@ def radial_basis_shard(modes, rho_global, world: int, rank: int, deriv_order: in
     ms = as_mode_set(modes)
     n, m = mode_arrays(ms)
     lo, hi = shard_range(len(rho_global), world, rank)
-    dev = rank if device is None else device
+    if device is None:  # this process's GPU: the local rank under torchrun
+        device = dist_env()[2] if "LOCAL_RANK" in os.environ else torch.cuda.current_device()
+    dev = int(device)
     rho = torch.as_tensor(radial_grid(rho_global[lo:hi]), dtype=torch.float64, device=f"cuda:{dev}")
     P, M = rho.numel(), len(ms)
     out = torch.empty((M, P), dtype=torch.float64, device=rho.device)
     if P and M:
         ctx = _lib.context(dev)
-        ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+        ctx.use_torch_stream(dev)
         plan = _lib.plan_for(ctx, n, m)
         _lib.check(_lib.lib.zk_radial_eval(ctx.handle, plan.handle, rho.data_ptr(), P,
                                            int(deriv_order), 0, out.data_ptr(), P, 0,

@@ -18,7 +18,7 @@ HEADER = os.path.join(ROOT, "include", "zk_b200.h")
 
 def header_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:const\s+char\s*\*|int)\s+(zk_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const\s+char\s*\*|int64_t|int)\s+(zk_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():

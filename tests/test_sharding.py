@@ -111,3 +111,86 @@ def test_sharded_fit_on_the_gpu_two_ranks(tmp_path):
     coef = np.load(tmp_path / "coef.npy")
     assert np.array_equal(x0, x1)
     assert np.abs(x0 - coef).max() <= 1e-9
+
+
+def test_packed_normal_equations_round_trip_cpu():
+    """K5 wire format on CPU tensors: [upper(G) column-major | r], M(M+1)/2 + M
+    doubles, and unpack restores the full symmetric G bit for bit."""
+    from paper_2409_19156_b200 import _lib
+    from paper_2409_19156_b200.series import pack_normal_equations, unpack_normal_equations
+    rng = np.random.default_rng(3)
+    for M in (1, 2, 7, 64):
+        A = rng.standard_normal((M, M))
+        G = torch.from_numpy(A + A.T)
+        r = torch.from_numpy(rng.standard_normal(M))
+        packed = pack_normal_equations(G, r)
+        assert packed.numel() == M * (M + 1) // 2 + M == _lib.lib.zk_gram_packed_count(M)
+        # column j of the upper triangle starts at j(j+1)/2
+        for j in range(M):
+            assert torch.equal(packed[j * (j + 1) // 2: j * (j + 1) // 2 + j + 1], G[: j + 1, j])
+        G2, r2 = unpack_normal_equations(packed, M)
+        assert torch.equal(G2, G) and torch.equal(r2, r)
+
+
+@pytest.mark.gpu
+def test_packed_normal_equations_gpu_kernels_match_cpu():
+    from paper_2409_19156_b200.series import pack_normal_equations, unpack_normal_equations
+    rng = np.random.default_rng(4)
+    for M in (1, 5, 300, 1891):
+        A = rng.standard_normal((M, M))
+        G = torch.from_numpy(A + A.T)
+        r = torch.from_numpy(rng.standard_normal(M))
+        pc = pack_normal_equations(G, r)
+        pg = pack_normal_equations(G.cuda(), r.cuda())
+        assert torch.equal(pg.cpu(), pc)
+        G2, r2 = unpack_normal_equations(pg, M)
+        assert torch.equal(G2.cpu(), G) and torch.equal(r2.cpu(), r)
+
+
+@pytest.mark.gpu
+def test_library_nccl_allreduce_single_process():
+    """zk_gram_allreduce (ncclCommInitAll clique over the visible devices) and
+    the one-process-per-GPU communicator (zk_comm_*), at the box's device count
+    (1 here: NCCL with one rank must return the input sum unchanged), and
+    gram(parallel=True) -- per-GPU K4 partials summed through the library's
+    NCCL path -- against the one-GPU gram."""
+    import ctypes
+
+    import paper_2409_19156_b200 as zb
+    from paper_2409_19156_b200 import _lib
+    assert _lib.nccl_version() >= 21800
+    rng = np.random.default_rng(6)
+    M = 97
+    A = rng.standard_normal((M, M))
+    G = torch.from_numpy(A + A.T).cuda()
+    r = torch.from_numpy(rng.standard_normal(M)).cuda()
+    G0, r0 = G.clone(), r.clone()
+    ctx = _lib.context(0)
+    ctx.set_stream(None)
+    arr = ctypes.c_void_p * 1
+    _lib.check(_lib.lib.zk_gram_allreduce(arr(ctx.handle.value), 1, arr(G.data_ptr()),
+                                          arr(r.data_ptr()), M, 0), "zk_gram_allreduce")
+    assert torch.equal(G, G0) and torch.equal(r, r0)
+    comm = _lib.Comm(ctx, _lib.Comm.unique_id(), 1, 0)
+    assert comm.info() == (1, 0)
+    G1, r1 = zb.allreduce_normal_equations(G.clone(), r.clone(), comm=comm)
+    torch.cuda.synchronize()
+    assert torch.equal(G1, G0) and torch.equal(r1, r0)
+    del comm
+
+    modes = zb.full_mode_set(16)
+    P = 20_000
+    rho = np.sqrt(rng.uniform(size=P))
+    theta = 2 * np.pi * rng.uniform(size=P)
+    c = rng.standard_normal(len(modes))
+    y = zb.series_eval(modes, c, rho, theta)
+    Gs, bs = zb.gram(modes, rho, theta, y)
+    Gp, bp = zb.gram(modes, rho, theta, y, parallel=True)
+    if len(zb.evaluate.parallel_devices()) == 1:
+        assert np.array_equal(Gp, Gs) and np.array_equal(bp, bs)
+    else:
+        assert np.abs(Gp - Gs).max() <= 1e-12 * np.abs(Gs).max()
+    x = zb.fit(modes, rho, theta, y, parallel=True)
+    assert np.abs(x - c).max() <= 1e-9
+    fp = zb.series_eval(modes, c, rho, theta, parallel=True)
+    assert np.array_equal(fp, y)
