@@ -135,6 +135,23 @@ def cr_power(rho: np.ndarray, e: int) -> np.ndarray:
     return np.array([float(Fraction(float(r)) ** e) for r in np.ravel(rho)]).reshape(np.shape(rho))
 
 
+def cached_cr_power(grid: np.ndarray):
+    """``cr_power`` memoised per exponent for one fixed grid: a big request
+    (thousands of keys at the same points) asks for each exponent many times."""
+    base = np.atleast_1d(np.asarray(grid, dtype=np.float64))
+    fr = [Fraction(float(r)) for r in base]
+    cache: dict[int, np.ndarray] = {}
+
+    def power(rho: np.ndarray, e: int) -> np.ndarray:
+        if rho is not base and not np.array_equal(rho, base):
+            return cr_power(rho, e)
+        if e not in cache:
+            cache[e] = np.array([float(f ** e) for f in fr], dtype=np.float64)
+        return cache[e]
+
+    return power
+
+
 def assemble(rho: np.ndarray, m: int, j: int, k: int, ch, power=numpy_power) -> np.ndarray:
     """zk/evaluate.py:102-154. ``ch[i]`` = P_{j-i}^{(m+i, i)}(u).
 

@@ -785,7 +785,8 @@ int zk_plan_create(zk_ctx* ctx, const int32_t* mode_n, const int32_t* mode_m, in
   size_t off_cols = align_up(off_rowptr + h.rowptr.size() * 4, A);
   size_t off_coef = align_up(off_cols + h.cols.size() * 4, A);
   size_t off_asm = align_up(off_coef + h.coef.size() * sizeof(zk::ChainCoef), A);
-  size_t total = align_up(off_asm + h.asmc.size() * sizeof(zk::AsmCoef), A) + A;
+  size_t off_tol = align_up(off_asm + h.asmc.size() * sizeof(zk::AsmCoef), A);
+  size_t total = align_up(off_tol + h.tol.size() * sizeof(zk::TolCoef), A) + A;
   std::vector<unsigned char> blob(total, 0);
   auto put = [&](size_t off, const void* src, size_t bytes) {
     if (bytes) std::memcpy(blob.data() + off, src, bytes);
@@ -796,6 +797,7 @@ int zk_plan_create(zk_ctx* ctx, const int32_t* mode_n, const int32_t* mode_m, in
   put(off_cols, h.cols.data(), h.cols.size() * 4);
   put(off_coef, h.coef.data(), h.coef.size() * sizeof(zk::ChainCoef));
   put(off_asm, h.asmc.data(), h.asmc.size() * sizeof(zk::AsmCoef));
+  put(off_tol, h.tol.data(), h.tol.size() * sizeof(zk::TolCoef));
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e == cudaSuccess) e = cudaMalloc(&plan->dmem, total);
   if (e == cudaSuccess) e = cudaMemcpy(plan->dmem, blob.data(), total, cudaMemcpyHostToDevice);
@@ -811,6 +813,7 @@ int zk_plan_create(zk_ctx* ctx, const int32_t* mode_n, const int32_t* mode_m, in
   plan->cols = reinterpret_cast<const int32_t*>(base + off_cols);
   plan->coef = reinterpret_cast<const zk::ChainCoef*>(base + off_coef);
   plan->asmc = reinterpret_cast<const zk::AsmCoef*>(base + off_asm);
+  plan->tol = reinterpret_cast<const zk::TolCoef*>(base + off_tol);
   *out = plan;
   return ZK_OK;
 }
@@ -910,6 +913,7 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const do
     a.cols = plan->cols;
     a.coef = plan->coef;
     a.asmc = plan->asmc;
+    a.tol = plan->tol;
     a.rho = d_rho;
     a.theta = d_theta;
     a.c = d_coef;
@@ -918,6 +922,8 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const do
     a.f = d_f;
     a.ldf = d_ldf;
     a.P = P;
+    a.exact = env_int("ZK_SERIES_EXACT", 0) != 0 ? 1 : 0;
+    a.max_smem = static_cast<int>(ctx->max_smem);
     const int64_t nrowslots = static_cast<int64_t>(plan->host.rowptr.size());
     rc = ensure_scratch(ctx, 1, zk::series_scratch_bytes(nrowslots));
     if (rc) return rc;
@@ -928,12 +934,6 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const do
     const bool dmma = (dm < 0 ? ncoef >= 8 : dm != 0) &&
                       zk::series_dmma_smem_bytes(deriv_order, plan->host.max_jmax, nch) <=
                           ctx->max_smem;
-    if (!dmma && zk::series_fma_smem_bytes(deriv_order, plan->host.max_jmax) > ctx->max_smem)
-      return fail(ZK_EINVAL,
-                  "series: jacobi degree " + std::to_string(plan->host.max_jmax) +
-                      " is too long for the series kernel's shared-memory stage at order " +
-                      std::to_string(deriv_order) +
-                      "; evaluate the basis (zk_radial_eval / zk_zernike_eval) and contract it");
     cudaError_t e = zk::launch_series(a, deriv_order, plan->host.max_jmax, nrowslots,
                                       static_cast<double*>(ctx->scratch[1]), dmma, st, &launches);
     ctx->launches += launches;

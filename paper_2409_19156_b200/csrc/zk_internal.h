@@ -21,6 +21,14 @@ struct alignas(16) ChainCoef {
 };
 static_assert(sizeof(ChainCoef) == 48, "ChainCoef layout");
 
+// Tolerance-mode form of the same step (series kernel, zk_series.cu):
+// P_j = (a x + b) P_{j-1} - c P_{j-2} with a = mid_x/lead, b = mid_const/lead,
+// c = last/lead, each the correctly rounded quotient of exact integers.
+struct alignas(16) TolCoef {
+  double a, b, c, pad;
+};
+static_assert(sizeof(TolCoef) == 32, "TolCoef layout");
+
 // Derivative prefactors per jacobi degree j of a group (zk/evaluate.py:127-149);
 // every product is an exact integer or half-integer in binary64.
 struct alignas(16) AsmCoef {
@@ -64,6 +72,7 @@ struct HostPlan {
   std::vector<int32_t> rowptr;        // per group jmax+2 entries, into cols
   std::vector<int32_t> cols;          // column*2 + (m < 0)
   std::vector<ChainCoef> coef;        // per group: (max_order+1) x (jmax+1)
+  std::vector<TolCoef> tol;           // same indexing as coef
   std::vector<AsmCoef> asmc;          // per group: (jmax+1)
 };
 

@@ -46,6 +46,7 @@ struct SeriesArgs {
   const int32_t* cols;
   const ChainCoef* coef;
   const AsmCoef* asmc;
+  const TolCoef* tol;     // tolerance-mode coefficients (same indexing as coef)
   const double* rho;
   const double* theta;    // nullptr: radial basis
   const double* c;        // M x ncoef, column-major, ldc
@@ -54,11 +55,13 @@ struct SeriesArgs {
   double* f;              // P x ncoef, column-major, ldf
   long long ldf;
   long long P;
+  int exact;              // 1: K1-identical recursion/assembly; 0: tolerance mode (FMA)
+  int max_smem;           // opt-in shared memory per block (bytes)
 };
 
 size_t series_scratch_bytes(long long nrowslots);
-// shared memory the FMA series kernel needs for one coefficient vector
-size_t series_fma_smem_bytes(int K, int max_jmax);
+// shared memory the FMA series kernel needs for nc coefficient vectors per launch
+size_t series_fma_smem_bytes(int K, int max_jmax, int nc, bool exact);
 cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nrowslots,
                           double* rowc, bool dmma, cudaStream_t st, int* launches);
 int series_dmma_chunks(int ncoef);

@@ -208,6 +208,7 @@ std::string build_plan(const int32_t* n, const int32_t* m, int64_t M, int max_or
       const int64_t a = g.alpha + i, b = i;
       for (int64_t j = 0; j <= g.jmax; ++j) {
         ChainCoef cc{};
+        TolCoef tc{};
         if (j >= 2) {
           const int64_t c = 2 * j + a + b;
           const int64_t lead = 2 * j * (c - j) * (c - 2);
@@ -216,8 +217,12 @@ std::string build_plan(const int32_t* n, const int32_t* m, int64_t M, int max_or
           cc.last = static_cast<double>(2 * (j + a - 1) * (j + b - 1) * c);
           cc.lead = static_cast<double>(lead);
           cc.rcp_lead = 1.0 / cc.lead;  // correctly rounded (IEEE division)
+          tc.a = cc.mid_x / cc.lead;
+          tc.b = cc.mid_const / cc.lead;
+          tc.c = cc.last / cc.lead;
         }
         P.coef.push_back(cc);
+        P.tol.push_back(tc);
       }
     }
     g.asm_off = static_cast<int32_t>(P.asmc.size());

@@ -26,6 +26,18 @@
 // accumulates X += R C+ and Y += R C- over the group's keys, and per group
 // f += X cos(|m| theta) + Y sin(|m| theta) -- no per-column work at all.
 // Only the summation order differs from B @ c (tolerance-equal).
+//
+// Tolerance-mode recursion (TOL, the default; ZK_SERIES_EXACT=1 selects the
+// K1-identical arithmetic): the series is a contraction whose summation
+// order already differs from B @ c, so bitwise reproduction of each basis
+// value buys nothing here. The plan carries the prescaled coefficients
+// a = mid_x/lead, b = mid_const/lead, c = last/lead (TolCoef, correctly
+// rounded quotients of the exact integers), and a chain step is P_j = fma(fma(a, x, b), P_{j-1}, -c P_{j-2})
+// -- 3 FP64 instructions instead of the exact path's 8 (no Markstein
+// division). For k = 0 the group's rho^|m| is constant over the group's
+// keys, so it multiplies the two group sums once instead of every value:
+// 5 FP64 instructions per (key, point) in all, vs 11. The error against
+// binary128 is measured in tests/test_gpu_series.py (n = 60, 100).
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -77,9 +89,48 @@ __global__ void series_rowsum_kernel(const GroupRec* __restrict__ groups,
   }
 }
 
-template <int K, bool ANG, int NC>
+// the tolerance-mode chain step: P_j = (a x + b) P_{j-1} - c P_{j-2}
+__device__ __forceinline__ TolCoef load_tol(const double* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 x = q[0], y = q[1];
+  return TolCoef{x.x, x.y, y.x, 0.0};
+}
+
+__device__ __forceinline__ double jacobi_step_tol(const TolCoef& c, double x, double p1,
+                                                  double p0) {
+  return fma(fma(c.a, x, c.b), p1, -(c.c * p0));
+}
+
+// assembly of zk/evaluate.py:124-149 with FMA contraction (tolerance mode)
+template <int K>
+__device__ __forceinline__ double assemble_tol(const PowSet<K>& s, const AsmCoef& a,
+                                               const double* ch) {
+  if constexpr (K == 0) {
+    return s.A0 * ch[0];
+  } else if constexpr (K == 1) {
+    return fma(s.A1, ch[0], -(a.c11 * s.B1) * ch[1]);
+  } else if constexpr (K == 2) {
+    const double t = fma(-(a.c21 * s.B2), ch[1], s.A2 * ch[0]);
+    return fma(a.c22 * s.C2, ch[2], t);
+  } else {
+    double t = fma(-(a.c31 * s.B3), ch[1], s.A3 * ch[0]);
+    t = fma(a.c32 * s.C3, ch[2], t);
+    return fma(-(a.c33 * s.D3), ch[3], t);
+  }
+}
+
+// Arithmetic / staging modes of the series kernel
+constexpr int kExact = 0;   // K1-identical recursion, tables staged in smem
+constexpr int kTol = 1;     // tolerance-mode recursion, prescaled tables in smem
+constexpr int kGlobal = 2;  // K1-identical, tables read from global memory
+                            // (chains too long for the smem stage: any degree)
+
+template <int K, bool ANG, int NC, int MODE>
 __global__ void __launch_bounds__(kThreads, 3)
 series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int buf_doubles) {
+  constexpr bool TOL = MODE == kTol;
+  constexpr bool GLB = MODE == kGlobal;
+  constexpr int CS = TOL ? 4 : 6;  // doubles per staged chain coefficient
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x;
   const long long p0 = static_cast<long long>(blockIdx.x) * kTile + tid * kVec;
@@ -117,12 +168,18 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
 
   // stage group gi's coefficients, prefactors and row pointers into buffer b
   auto stage = [&](int gi, int b) {
+    if constexpr (GLB) return;
     const GroupRec g = a.groups[gi];
     const int nj = g.jmax + 1;
     double* base = smem + b * buf_doubles;
-    const double* csrc = reinterpret_cast<const double*>(a.coef + g.coef_off);
-    const int ncoef = (K + 1) * nj * 6;
-    for (int t = tid; t < ncoef; t += kThreads) cp_async8(base + t, csrc + t);
+    const int ncoef = (K + 1) * nj * CS;
+    if constexpr (TOL) {  // the plan's prescaled coefficients (TolCoef)
+      const double* tsrc = reinterpret_cast<const double*>(a.tol + g.coef_off);
+      for (int t = tid; t < ncoef; t += kThreads) cp_async8(base + t, tsrc + t);
+    } else {
+      const double* csrc = reinterpret_cast<const double*>(a.coef + g.coef_off);
+      for (int t = tid; t < ncoef; t += kThreads) cp_async8(base + t, csrc + t);
+    }
     double* abase = base + ncoef;
     if (K > 0) {
       const double* asrc = reinterpret_cast<const double*>(a.asmc + g.asm_off);
@@ -134,20 +191,33 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  stage(0, 0);
+  if constexpr (!GLB) stage(0, 0);
   for (int gi = 0; gi < a.ngroups; ++gi) {
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();  // buffer gi&1 ready; everyone is done with buffer (gi+1)&1
-    if (gi + 1 < a.ngroups) stage(gi + 1, (gi + 1) & 1);
+    if constexpr (!GLB) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncthreads();  // buffer gi&1 ready; everyone is done with buffer (gi+1)&1
+      if (gi + 1 < a.ngroups) stage(gi + 1, (gi + 1) & 1);
+    }
 
     const GroupRec g = a.groups[gi];
     const int alpha = g.alpha;
     const int jmax = g.jmax;
     const int nj = jmax + 1;
     const double* base = smem + (gi & 1) * buf_doubles;
-    const ChainCoef* s_coef = reinterpret_cast<const ChainCoef*>(base);
-    const AsmCoef* s_asm = reinterpret_cast<const AsmCoef*>(base + (K + 1) * nj * 6);
-    const double* s_rc = base + (K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0);
+    const ChainCoef* s_coef =
+        GLB ? a.coef + g.coef_off : reinterpret_cast<const ChainCoef*>(base);
+    const AsmCoef* s_asm =
+        GLB ? a.asmc + g.asm_off : reinterpret_cast<const AsmCoef*>(base + (K + 1) * nj * CS);
+    const double* s_rc = GLB ? rowc + static_cast<long long>(g.row0) * 2 * NC
+                             : base + (K + 1) * nj * CS + (K > 0 ? nj * 8 : 0);
+    // chain step of chain i to degree d (exact or tolerance mode)
+    auto step_at = [&](int i, int d, double x, double p1, double p0) {
+      if constexpr (TOL) {
+        return jacobi_step_tol(load_tol(base + (i * nj + d) * 4), x, p1, p0);
+      } else {
+        return jacobi_step(load_coef(s_coef + i * nj + d), x, p1, p0);
+      }
+    };
 
     // rho powers: advance the double-double accumulator to rho^base (alpha ascends)
     const int e_lo = powset_base<K>(alpha);
@@ -197,7 +267,12 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
 #pragma unroll
         for (int i = 0; i <= K; ++i)
           ch[i] = (decltype(steady)::value || j - i >= 0) ? chs[i][v] : 0.0;
-        val[v] = assemble<K, K>(pw[v], ac, ch);
+        if constexpr (TOL && K == 0)
+          val[v] = ch[0];  // rho^|m| multiplies the group sums (below)
+        else if constexpr (TOL)
+          val[v] = assemble_tol<K>(pw[v], ac, ch);
+        else
+          val[v] = assemble<K, K>(pw[v], ac, ch);
       }
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -229,10 +304,9 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
             A[i][v] = jacobi_p1(a1, ab2, u[v]);
           }
         } else if (d >= 2) {
-          const ChainCoef c = load_coef(s_coef + i * nj + d);
 #pragma unroll
           for (int v = 0; v < kVec; ++v) {
-            const double nx = jacobi_step(c, u[v], A[i][v], B[i][v]);
+            const double nx = step_at(i, d, u[v], A[i][v], B[i][v]);
             B[i][v] = A[i][v];
             A[i][v] = nx;
           }
@@ -244,27 +318,33 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
     for (; j + 1 <= jmax; j += 2) {
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = load_coef(s_coef + i * nj + (j - i));
 #pragma unroll
-        for (int v = 0; v < kVec; ++v) B[i][v] = jacobi_step(c, u[v], A[i][v], B[i][v]);
+        for (int v = 0; v < kVec; ++v) B[i][v] = step_at(i, j - i, u[v], A[i][v], B[i][v]);
       }
       fold(j, B, std::true_type{});
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = load_coef(s_coef + i * nj + (j + 1 - i));
 #pragma unroll
-        for (int v = 0; v < kVec; ++v) A[i][v] = jacobi_step(c, u[v], B[i][v], A[i][v]);
+        for (int v = 0; v < kVec; ++v) A[i][v] = step_at(i, j + 1 - i, u[v], B[i][v], A[i][v]);
       }
       fold(j + 1, A, std::true_type{});
     }
     if (j <= jmax) {
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = load_coef(s_coef + i * nj + (j - i));
 #pragma unroll
-        for (int v = 0; v < kVec; ++v) B[i][v] = jacobi_step(c, u[v], A[i][v], B[i][v]);
+        for (int v = 0; v < kVec; ++v) B[i][v] = step_at(i, j - i, u[v], A[i][v], B[i][v]);
       }
       fold(j, B, std::true_type{});
+    }
+    if constexpr (TOL && K == 0) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int v = 0; v < kVec; ++v) {
+          gx[c][v] *= pw[v].A0;
+          if (ANG) gy[c][v] *= pw[v].A0;
+        }
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c)
@@ -290,7 +370,11 @@ static cudaError_t launch_one(const SeriesArgs& a, const double* rowc, int v0, i
                               cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>((a.P + kTile - 1) / kTile);
   const size_t smem = size_t(2) * buf_doubles * sizeof(double);
-  auto fn = series_kernel<K, ANG, NC>;
+  auto fn = a.exact ? series_kernel<K, ANG, NC, kExact> : series_kernel<K, ANG, NC, kTol>;
+  if (buf_doubles == 0) {  // long chains: global-table variant, one vector per launch
+    if constexpr (NC != 1) return cudaErrorInvalidValue;
+    fn = series_kernel<K, ANG, 1, kGlobal>;
+  }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -318,10 +402,14 @@ static cudaError_t launch_ang(const SeriesArgs& a, const double* rowc, int v0, i
                  : launch_nc<K, false>(a, rowc, v0, nc, buf_doubles, st);
 }
 
-size_t series_fma_smem_bytes(int K, int max_jmax) {
-  const int nj = max_jmax + 1;
-  const int buf = ((K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0) + nj * 2 + 1) & ~1;  // nc = 1
-  return size_t(2) * buf * sizeof(double);
+// doubles of one group's stage: (K+1) x nj chain coefficients, nj AsmCoef,
+// nj x 2nc row coefficients
+static int series_buf_doubles(int K, int nj, int nc, bool exact) {
+  return ((K + 1) * nj * (exact ? 6 : 4) + (K > 0 ? nj * 8 : 0) + nj * 2 * nc + 1) & ~1;
+}
+
+size_t series_fma_smem_bytes(int K, int max_jmax, int nc, bool exact) {
+  return size_t(2) * series_buf_doubles(K, max_jmax + 1, nc, exact) * sizeof(double);
 }
 
 size_t series_scratch_bytes(long long nrowslots) {
@@ -353,9 +441,12 @@ cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nr
   }
   for (int v0 = 0; v0 < a.ncoef;) {
     const int left = a.ncoef - v0;
-    const int nc = left >= 8 ? 8 : left >= 4 ? 4 : left >= 2 ? 2 : 1;
-    // per-group stage: (K+1) x nj ChainCoef, nj AsmCoef, nj x 2nc row coefficients
-    const int buf_doubles = ((K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0) + nj * 2 * nc + 1) & ~1;
+    int nc = left >= 8 ? 8 : left >= 4 ? 4 : left >= 2 ? 2 : 1;
+    // fewer vectors per launch when the stage of nc would not fit; chains too
+    // long for any stage read their tables from global memory (buf_doubles 0)
+    while (nc > 1 && series_fma_smem_bytes(K, max_jmax, nc, a.exact) > size_t(a.max_smem)) nc >>= 1;
+    const bool global = series_fma_smem_bytes(K, max_jmax, nc, a.exact) > size_t(a.max_smem);
+    const int buf_doubles = global ? 0 : series_buf_doubles(K, nj, nc, a.exact);
     if (a.theta)
       series_rowsum_kernel<true><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
                                                            a.ldc, v0, nc, nc, rowc);

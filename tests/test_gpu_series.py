@@ -134,10 +134,50 @@ def test_series_fma_and_dmma_paths(monkeypatch, path, k, V):
         assert (np.abs(f - ref) <= 1e-13 * scale + 1e-13).all(), (path, k, V, th is None)
 
 
-def test_series_too_long_chain_fails_with_clear_error():
-    modes = zb.as_mode_set([(3000, 0)])
-    with pytest.raises(ValueError, match="series kernel"):
-        zb.series_eval(modes, np.ones(1), np.array([0.5]), deriv_order=3)
+@pytest.mark.parametrize("V", [1, 3])
+def test_series_long_chains_any_degree(V):
+    """Chains whose tables exceed the shared-memory stage (n = 3000, k = 3)
+    run the global-table variant (the reference has no degree limit,
+    zk/evaluate.py:259-274); the stage of several vectors steps down first."""
+    modes = zb.as_mode_set([(3000, 0), (2999, -1), (2998, 2), (1200, 0), (7, 3)])
+    pairs = [(md.n, md.m) for md in modes]
+    rho = np.array([0.0, 0.1, 0.37, 0.5, 0.71, 0.93])
+    C = np.random.default_rng(V).standard_normal((len(modes), V))
+    for k in (0, 3):
+        f = zb.series_eval(modes, C, rho, None, k)
+        B = orc.radial_batch(pairs, rho, k)
+        scale = np.abs(B) @ np.abs(C)
+        assert (np.abs(f.reshape(rho.size, V) - B @ C) <= 1e-12 * scale + 1e-13).all(), k
+
+
+@pytest.mark.parametrize("N", [60, 100])
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_series_tolerance_mode_error_vs_binary128(monkeypatch, N, k):
+    """The series' default tolerance-mode recursion (prescaled coefficients,
+    FMA contraction) against the binary128 oracle (oracle/zk_quad.c, bitwise
+    the reference's exact oracle on every golden value), next to the exact
+    K1-identical arithmetic (ZK_SERIES_EXACT=1): error per point relative to
+    sum_col |B c| (2-D basis, fl(|m| theta) angles as zk/evaluate.py:272-274)."""
+    modes = zb.full_mode_set(N)
+    pairs = [(md.n, md.m) for md in modes]
+    rho, theta = disc(1500, N + k)
+    c = np.random.default_rng(k).standard_normal(len(modes))
+    Bq = orc.quad_table(pairs, rho, k)
+    m = np.array([md.m for md in modes])
+    ang = np.where(m >= 0, np.cos(np.abs(m)[None, :] * theta[:, None]),
+                   np.sin(np.abs(m)[None, :] * theta[:, None]))
+    B2 = Bq * ang
+    ref = (B2.astype(np.longdouble) @ c.astype(np.longdouble)).astype(np.float64)
+    scale = np.abs(B2) @ np.abs(c)
+    errs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("ZK_SERIES_EXACT", mode)
+        f = zb.series_eval(modes, c, rho, theta, k)
+        errs[mode] = float((np.abs(f - ref) / scale).max())
+    print(f"n<={N} k={k}: tolerance mode {errs['0']:.3e}, exact mode {errs['1']:.3e} "
+          f"(of sum|B||c|)")
+    assert errs["0"] <= 1e-13
+    assert errs["0"] <= 8 * errs["1"] + 1e-15
 
 
 def test_device_entry_points_reject_wrong_dtype_or_device():
