@@ -924,6 +924,12 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const do
     a.P = P;
     a.exact = env_int("ZK_SERIES_EXACT", 0) != 0 ? 1 : 0;
     a.max_smem = static_cast<int>(ctx->max_smem);
+    a.sms = ctx->sm_count;
+    a.resident = env_int("ZK_SERIES_RESIDENT", 0);
+    a.vec3 = env_int("ZK_SERIES_VEC3", 1);
+    a.ntol = static_cast<int>(plan->host.tol.size());
+    a.nasm = static_cast<int>(plan->host.asmc.size());
+    a.nrows = static_cast<int>(plan->host.rowptr.size());
     const int64_t nrowslots = static_cast<int64_t>(plan->host.rowptr.size());
     rc = ensure_scratch(ctx, 1, zk::series_scratch_bytes(nrowslots));
     if (rc) return rc;

@@ -57,6 +57,10 @@ struct SeriesArgs {
   long long P;
   int exact;              // 1: K1-identical recursion/assembly; 0: tolerance mode (FMA)
   int max_smem;           // opt-in shared memory per block (bytes)
+  int sms;                // SM count
+  int resident;           // allow the whole-plan resident stage (tolerance mode)
+  int vec3;               // 3 points per thread for the k = 0 single-vector kernel
+  int ntol, nasm, nrows;  // plan table sizes: TolCoef/ChainCoef, AsmCoef, row slots
 };
 
 size_t series_scratch_bytes(long long nrowslots);

@@ -49,8 +49,7 @@ namespace zk {
 
 namespace {
 constexpr int kThreads = 256;
-constexpr int kVec = 2;
-constexpr int kTile = kThreads * kVec;
+constexpr int kMaxVec = 3;  // points per thread: 2, or 3 for the k = 0 single-vector kernel
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -119,56 +118,102 @@ __device__ __forceinline__ double assemble_tol(const PowSet<K>& s, const AsmCoef
   }
 }
 
+// parked per-thread fields (see series_kernel)
+constexpr int kRho = 0, kTh = 1, kPwHi = 2, kPwLo = 3, kC1 = 4, kS1 = 5, kCs = 6, kSn = 7;
+constexpr int kPark = 8;
+
 // Arithmetic / staging modes of the series kernel
 constexpr int kExact = 0;   // K1-identical recursion, tables staged in smem
 constexpr int kTol = 1;     // tolerance-mode recursion, prescaled tables in smem
 constexpr int kGlobal = 2;  // K1-identical, tables read from global memory
                             // (chains too long for the smem stage: any degree)
+constexpr int kResident = 3;  // tolerance mode, the WHOLE plan's tables staged
+                              // once per CTA: no per-group barrier; persistent
+                              // CTAs walk several point tiles
 
-template <int K, bool ANG, int NC, int MODE>
-__global__ void __launch_bounds__(kThreads, 3)
+// CTAs per SM the register budget is sized for: the k = 0, few-vector
+// kernels fit 64 registers once the group state is parked (4 CTAs, 32 warps)
+template <int K, int NC, int VEC>
+constexpr int series_min_blocks() {
+  return (K == 0 && NC <= 2 && VEC == 2) ? 4 : 3;
+}
+
+template <int K, bool ANG, int NC, int MODE, int VEC>
+__global__ void __launch_bounds__(kThreads, series_min_blocks<K, NC, VEC>())
 series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int buf_doubles) {
-  constexpr bool TOL = MODE == kTol;
+  constexpr bool RES = MODE == kResident;
+  constexpr bool TOL = MODE == kTol || RES;
   constexpr bool GLB = MODE == kGlobal;
+  constexpr bool STAGED = !GLB && !RES;  // per-group double-buffered stage
   constexpr int CS = TOL ? 4 : 6;  // doubles per staged chain coefficient
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(16) double smem_all[];
+  // per-thread group-level state parked in shared memory while the steady
+  // loop runs (frees ~30 registers for the chains, the sums and the
+  // coefficient loads in flight): field f of point v at park[(f VEC + v) T + tid]
+  double* park = smem_all;
+  double* smem = smem_all + kPark * VEC * kThreads;
   const int tid = threadIdx.x;
-  const long long p0 = static_cast<long long>(blockIdx.x) * kTile + tid * kVec;
-
-  double rho[kVec], u[kVec], th[kVec];
-  dd pw_acc[kVec];
-#pragma unroll
-  for (int v = 0; v < kVec; ++v) {
-    const bool live = p0 + v < a.P;
-    rho[v] = live ? __ldg(a.rho + p0 + v) : 0.0;
-    th[v] = (ANG && live) ? __ldg(a.theta + p0 + v) : 0.0;
-    u[v] = jacobi_u(rho[v]);
-    pw_acc[v] = dd{1.0, 0.0};
+  auto pk = [&](int f, int v) -> double& { return park[(f * VEC + v) * kThreads + tid]; };
+  // resident layout: [TolCoef of chains 0..K, group after group (nasm x (K+1))
+  //                   | AsmCoef x nasm (K > 0) | rowc x nrows]
+  const double* r_asm = smem + 4 * (K + 1) * a.nasm;
+  const double* r_rc = r_asm + (K > 0 ? 8 * a.nasm : 0);
+  if constexpr (RES) {
+    const double* tsrc = reinterpret_cast<const double*>(a.tol);
+    int toff = 0;
+    for (int gi = 0; gi < a.ngroups; ++gi) {  // the plan holds chains 0..3: keep 0..K
+      const GroupRec g = a.groups[gi];
+      const int n = 4 * (K + 1) * (g.jmax + 1);
+      for (int t = tid; t < n; t += kThreads)
+        cp_async8(smem + toff + t, tsrc + 4LL * g.coef_off + t);
+      toff += n;
+    }
+    if (K > 0) {
+      const double* asrc = reinterpret_cast<const double*>(a.asmc);
+      for (int t = tid; t < 8 * a.nasm; t += kThreads)
+        cp_async8(const_cast<double*>(r_asm) + t, asrc + t);
+    }
+    for (int t = tid; t < 2 * NC * a.nrows; t += kThreads)
+      cp_async8(const_cast<double*>(r_rc) + t, rowc + t);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
   }
-  int e_cur = 0;
+  const long long ntiles = (a.P + (kThreads * VEC) - 1) / (kThreads * VEC);
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const long long p0 = tile * (kThreads * VEC) + tid * VEC;
+
   // angular factors cos/sin(alpha theta) for the ascending groups: exact
   // sincos(fl(alpha theta)) at an anchor, then rotations by theta for small
   // alpha steps (<= 4 per group, <= 8 since the anchor: ~1e-15 relative,
   // far inside the series tolerance); saves most of the per-group sincos
-  double c1[kVec], s1[kVec], cs_a[kVec], sn_a[kVec];
-  int a_cur = -1, since = 0;
 #pragma unroll
-  for (int v = 0; v < kVec; ++v) {
-    c1[v] = 1.0;
-    s1[v] = 0.0;
-    cs_a[v] = 1.0;
-    sn_a[v] = 0.0;
-    if (ANG) sincos(th[v], &s1[v], &c1[v]);
+  for (int v = 0; v < VEC; ++v) {
+    const bool live = p0 + v < a.P;
+    const double r = live ? __ldg(a.rho + p0 + v) : 0.0;
+    const double t = (ANG && live) ? __ldg(a.theta + p0 + v) : 0.0;
+    double c1 = 1.0, s1 = 0.0;
+    if (ANG) sincos(t, &s1, &c1);
+    pk(kRho, v) = r;
+    pk(kTh, v) = t;
+    pk(kPwHi, v) = 1.0;
+    pk(kPwLo, v) = 0.0;
+    pk(kC1, v) = c1;
+    pk(kS1, v) = s1;
+    pk(kCs, v) = 1.0;
+    pk(kSn, v) = 0.0;
   }
-  double acc[NC][kVec];
+  int e_cur = 0;
+  int a_cur = -1, since = 0;
+  double acc[NC][VEC];
 #pragma unroll
   for (int c = 0; c < NC; ++c)
 #pragma unroll
-    for (int v = 0; v < kVec; ++v) acc[c][v] = 0.0;
+    for (int v = 0; v < VEC; ++v) acc[c][v] = 0.0;
 
   // stage group gi's coefficients, prefactors and row pointers into buffer b
   auto stage = [&](int gi, int b) {
-    if constexpr (GLB) return;
+    if constexpr (!STAGED) return;
     const GroupRec g = a.groups[gi];
     const int nj = g.jmax + 1;
     double* base = smem + b * buf_doubles;
@@ -191,9 +236,10 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  if constexpr (!GLB) stage(0, 0);
+  if constexpr (STAGED) stage(0, 0);
+  int r_toff = 0;  // resident: this group's TolCoef offset (doubles)
   for (int gi = 0; gi < a.ngroups; ++gi) {
-    if constexpr (!GLB) {
+    if constexpr (STAGED) {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();  // buffer gi&1 ready; everyone is done with buffer (gi+1)&1
       if (gi + 1 < a.ngroups) stage(gi + 1, (gi + 1) & 1);
@@ -203,13 +249,17 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
     const int alpha = g.alpha;
     const int jmax = g.jmax;
     const int nj = jmax + 1;
-    const double* base = smem + (gi & 1) * buf_doubles;
+    const double* base = RES ? smem + r_toff : smem + (gi & 1) * buf_doubles;
+    r_toff += 4 * (K + 1) * nj;
     const ChainCoef* s_coef =
         GLB ? a.coef + g.coef_off : reinterpret_cast<const ChainCoef*>(base);
     const AsmCoef* s_asm =
-        GLB ? a.asmc + g.asm_off : reinterpret_cast<const AsmCoef*>(base + (K + 1) * nj * CS);
+        GLB ? a.asmc + g.asm_off
+            : RES ? reinterpret_cast<const AsmCoef*>(r_asm) + g.asm_off
+                  : reinterpret_cast<const AsmCoef*>(base + (K + 1) * nj * CS);
     const double* s_rc = GLB ? rowc + static_cast<long long>(g.row0) * 2 * NC
-                             : base + (K + 1) * nj * CS + (K > 0 ? nj * 8 : 0);
+                         : RES ? r_rc + static_cast<long long>(g.row0) * 2 * NC
+                               : base + (K + 1) * nj * CS + (K > 0 ? nj * 8 : 0);
     // chain step of chain i to degree d (exact or tolerance mode)
     auto step_at = [&](int i, int d, double x, double p1, double p0) {
       if constexpr (TOL) {
@@ -221,29 +271,47 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
 
     // rho powers: advance the double-double accumulator to rho^base (alpha ascends)
     const int e_lo = powset_base<K>(alpha);
-    PowSet<K> pw[kVec];
+    PowSet<K> pw[VEC];
+    double u[VEC];
 #pragma unroll
-    for (int v = 0; v < kVec; ++v) {
-      if (e_lo > e_cur) pw_acc[v] = dd_mul(pw_acc[v], dd_pow(rho[v], e_lo - e_cur));
-      pw[v] = make_powset_from<K>(pw_acc[v], rho[v], alpha);
+    for (int v = 0; v < VEC; ++v) {
+      const double r = pk(kRho, v);
+      u[v] = jacobi_u(r);
+      dd acc_p{pk(kPwHi, v), pk(kPwLo, v)};
+      if (e_lo == e_cur + 1)
+        acc_p = dd_mul_d(acc_p, r);
+      else if (e_lo > e_cur)
+        acc_p = dd_mul(acc_p, dd_pow(r, e_lo - e_cur));
+      pk(kPwHi, v) = acc_p.hi;
+      pk(kPwLo, v) = acc_p.lo;
+      // k = 0 tolerance mode: rho^|m| (= acc_p.hi) is read back at the group's end
+      if constexpr (!(TOL && K == 0)) pw[v] = make_powset_from<K>(acc_p, r, alpha);
     }
     e_cur = e_lo > e_cur ? e_lo : e_cur;
     if constexpr (ANG) {
       const int step = alpha - a_cur;  // CTA-uniform
       if (a_cur >= 0 && step <= 4 && since + step <= 8) {
-        for (int t = 0; t < step; ++t) {
 #pragma unroll
-          for (int v = 0; v < kVec; ++v) {
-            const double c = fma(cs_a[v], c1[v], -sn_a[v] * s1[v]);
-            sn_a[v] = fma(sn_a[v], c1[v], cs_a[v] * s1[v]);
-            cs_a[v] = c;
+        for (int v = 0; v < VEC; ++v) {
+          const double c1 = pk(kC1, v), s1 = pk(kS1, v);
+          double cs = pk(kCs, v), sn = pk(kSn, v);
+          for (int t = 0; t < step; ++t) {
+            const double c = fma(cs, c1, -sn * s1);
+            sn = fma(sn, c1, cs * s1);
+            cs = c;
           }
+          pk(kCs, v) = cs;
+          pk(kSn, v) = sn;
         }
         since += step;
       } else {
 #pragma unroll
-        for (int v = 0; v < kVec; ++v)
-          sincos(__dmul_rn(static_cast<double>(alpha), th[v]), &sn_a[v], &cs_a[v]);
+        for (int v = 0; v < VEC; ++v) {
+          double cs, sn;
+          sincos(__dmul_rn(static_cast<double>(alpha), pk(kTh, v)), &sn, &cs);
+          pk(kCs, v) = cs;
+          pk(kSn, v) = sn;
+        }
         since = 0;
       }
       a_cur = alpha;
@@ -251,18 +319,18 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
 
     // per-group sums: the angular factors are constant over a group, so they
     // multiply the group's two partial sums once (2 FMAs per key instead of 3)
-    double gx[NC][kVec], gy[NC][kVec];
+    double gx[NC][VEC], gy[NC][VEC];
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
-      for (int v = 0; v < kVec; ++v) gx[c][v] = gy[c][v] = 0.0;
+      for (int v = 0; v < VEC; ++v) gx[c][v] = gy[c][v] = 0.0;
     // fold degree j's value into the running sums; STEADY: all chains >= 2
-    auto fold = [&](int j, const double(&chs)[K + 1][kVec], auto steady) {
+    auto fold = [&](int j, const double(&chs)[K + 1][VEC], auto steady) {
       AsmCoef ac;
       if constexpr (K > 0) ac = load_asm(s_asm + j);
-      double val[kVec];
+      double val[VEC];
 #pragma unroll
-      for (int v = 0; v < kVec; ++v) {
+      for (int v = 0; v < VEC; ++v) {
         double ch[K + 1];
 #pragma unroll
         for (int i = 0; i <= K; ++i)
@@ -278,14 +346,14 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
       for (int c = 0; c < NC; ++c) {
         const double2 cpn = *reinterpret_cast<const double2*>(s_rc + (j * NC + c) * 2);
 #pragma unroll
-        for (int v = 0; v < kVec; ++v) {
+        for (int v = 0; v < VEC; ++v) {
           gx[c][v] = fma(val[v], cpn.x, gx[c][v]);  // the group's cos(|m| theta) part
           if (ANG) gy[c][v] = fma(val[v], cpn.y, gy[c][v]);  // its sin(|m| theta) part
         }
       }
     };
 
-    double A[K + 1][kVec], B[K + 1][kVec];  // A: newest degree, B: the one before
+    double A[K + 1][VEC], B[K + 1][VEC];  // A: newest degree, B: the one before
 #pragma unroll
     for (int j = 0; j <= K + 1; ++j) {  // prologue degrees, d-branches resolved at compile time
       if (j > jmax) break;
@@ -294,18 +362,18 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
         const int d = j - i;
         if (d == 0) {
 #pragma unroll
-          for (int v = 0; v < kVec; ++v) A[i][v] = 1.0;
+          for (int v = 0; v < VEC; ++v) A[i][v] = 1.0;
         } else if (d == 1) {
           const double a1 = static_cast<double>(alpha + i + 1);
           const double ab2 = static_cast<double>(alpha + 2 * i + 2);
 #pragma unroll
-          for (int v = 0; v < kVec; ++v) {
+          for (int v = 0; v < VEC; ++v) {
             B[i][v] = A[i][v];
             A[i][v] = jacobi_p1(a1, ab2, u[v]);
           }
         } else if (d >= 2) {
 #pragma unroll
-          for (int v = 0; v < kVec; ++v) {
+          for (int v = 0; v < VEC; ++v) {
             const double nx = step_at(i, d, u[v], A[i][v], B[i][v]);
             B[i][v] = A[i][v];
             A[i][v] = nx;
@@ -319,13 +387,13 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
 #pragma unroll
-        for (int v = 0; v < kVec; ++v) B[i][v] = step_at(i, j - i, u[v], A[i][v], B[i][v]);
+        for (int v = 0; v < VEC; ++v) B[i][v] = step_at(i, j - i, u[v], A[i][v], B[i][v]);
       }
       fold(j, B, std::true_type{});
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
 #pragma unroll
-        for (int v = 0; v < kVec; ++v) A[i][v] = step_at(i, j + 1 - i, u[v], B[i][v], A[i][v]);
+        for (int v = 0; v < VEC; ++v) A[i][v] = step_at(i, j + 1 - i, u[v], B[i][v], A[i][v]);
       }
       fold(j + 1, A, std::true_type{});
     }
@@ -333,47 +401,80 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
 #pragma unroll
-        for (int v = 0; v < kVec; ++v) B[i][v] = step_at(i, j - i, u[v], A[i][v], B[i][v]);
+        for (int v = 0; v < VEC; ++v) B[i][v] = step_at(i, j - i, u[v], A[i][v], B[i][v]);
       }
       fold(j, B, std::true_type{});
     }
     if constexpr (TOL && K == 0) {
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
+      for (int v = 0; v < VEC; ++v) {
+        const double a0 = pk(kPwHi, v);  // rho^|m|
 #pragma unroll
-        for (int v = 0; v < kVec; ++v) {
-          gx[c][v] *= pw[v].A0;
-          if (ANG) gy[c][v] *= pw[v].A0;
+        for (int c = 0; c < NC; ++c) {
+          gx[c][v] *= a0;
+          if (ANG) gy[c][v] *= a0;
         }
+      }
     }
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
+    for (int v = 0; v < VEC; ++v) {
+      const double cs = ANG ? pk(kCs, v) : 1.0, sn = ANG ? pk(kSn, v) : 0.0;
 #pragma unroll
-      for (int v = 0; v < kVec; ++v) {
+      for (int c = 0; c < NC; ++c) {
         if (ANG) {
-          acc[c][v] = fma(gx[c][v], cs_a[v], acc[c][v]);
-          acc[c][v] = fma(gy[c][v], sn_a[v], acc[c][v]);
+          acc[c][v] = fma(gx[c][v], cs, acc[c][v]);
+          acc[c][v] = fma(gy[c][v], sn, acc[c][v]);
         } else {
           acc[c][v] += gx[c][v];
         }
       }
+    }
   }
 #pragma unroll
   for (int c = 0; c < NC; ++c)
 #pragma unroll
-    for (int v = 0; v < kVec; ++v)
+    for (int v = 0; v < VEC; ++v)
       if (p0 + v < a.P) a.f[p0 + v + (v0 + c) * a.ldf] = acc[c][v];
+  }  // tiles
 }
 
-template <int K, bool ANG, int NC>
-static cudaError_t launch_one(const SeriesArgs& a, const double* rowc, int v0, int buf_doubles,
+// doubles of the resident layout (the whole plan's tables), 0 if unusable
+static long long resident_doubles(const SeriesArgs& a, int K, int nc) {
+  return 4LL * (K + 1) * a.nasm + (K > 0 ? 8LL * a.nasm : 0) + 2LL * nc * a.nrows;
+}
+
+template <int K, bool ANG, int NC, int VEC>
+static cudaError_t launch_vec(const SeriesArgs& a, const double* rowc, int v0, int buf_doubles,
                               cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>((a.P + kTile - 1) / kTile);
-  const size_t smem = size_t(2) * buf_doubles * sizeof(double);
-  auto fn = a.exact ? series_kernel<K, ANG, NC, kExact> : series_kernel<K, ANG, NC, kTol>;
+  constexpr int kTile = kThreads * VEC;
+  const long long ntiles = (a.P + kTile - 1) / kTile;
+  unsigned grid = static_cast<unsigned>(ntiles);
+  const size_t park = size_t(kPark) * VEC * kThreads * sizeof(double);
+  size_t smem = park + size_t(2) * buf_doubles * sizeof(double);
+  auto fn = a.exact ? series_kernel<K, ANG, NC, kExact, VEC> : series_kernel<K, ANG, NC, kTol, VEC>;
   if (buf_doubles == 0) {  // long chains: global-table variant, one vector per launch
-    if constexpr (NC != 1) return cudaErrorInvalidValue;
-    fn = series_kernel<K, ANG, 1, kGlobal>;
+    if constexpr (NC != 1 || VEC != 2) return cudaErrorInvalidValue;
+    fn = series_kernel<K, ANG, 1, kGlobal, 2>;
+  } else if (!a.exact && a.resident) {
+    // the whole plan fits: stage it once per CTA, persistent CTAs over the tiles
+    const size_t rs = park + size_t(resident_doubles(a, K, NC)) * sizeof(double);
+    if (rs <= size_t(a.max_smem)) {
+      auto rfn = series_kernel<K, ANG, NC, kResident, VEC>;
+      cudaError_t e = cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(rs));
+      int per_sm = 0;
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rfn, kThreads, rs);
+      if (e != cudaSuccess) return e;
+      if (per_sm >= 2) {
+        fn = rfn;
+        smem = rs;
+        const long long slots = static_cast<long long>(per_sm) * a.sms;
+        // whole waves of tiles: ceil(ntiles / slots) tiles per CTA, spread evenly
+        const long long per_cta = (ntiles + slots - 1) / slots;
+        grid = static_cast<unsigned>((ntiles + per_cta - 1) / per_cta);
+      }
+    }
   }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -382,6 +483,18 @@ static cudaError_t launch_one(const SeriesArgs& a, const double* rowc, int v0, i
   }
   fn<<<grid, kThreads, smem, st>>>(a, rowc, v0, buf_doubles);
   return cudaGetLastError();
+}
+
+template <int K, bool ANG, int NC>
+static cudaError_t launch_one(const SeriesArgs& a, const double* rowc, int v0, int buf_doubles,
+                              cudaStream_t st) {
+  // 3 points per thread for the k = 0 single-vector kernel: the per-key
+  // shared-memory loads serve 3 points, and 1e6-point requests fill whole
+  // waves (2.9 of 444 CTA slots vs 4.4)
+  if constexpr (K == 0 && NC == 1)
+    if (!a.exact && buf_doubles > 0 && a.vec3)
+      return launch_vec<K, ANG, NC, 3>(a, rowc, v0, buf_doubles, st);
+  return launch_vec<K, ANG, NC, 2>(a, rowc, v0, buf_doubles, st);
 }
 
 template <int K, bool ANG>
@@ -409,7 +522,9 @@ static int series_buf_doubles(int K, int nj, int nc, bool exact) {
 }
 
 size_t series_fma_smem_bytes(int K, int max_jmax, int nc, bool exact) {
-  return size_t(2) * series_buf_doubles(K, max_jmax + 1, nc, exact) * sizeof(double);
+  return (size_t(kPark) * kMaxVec * kThreads +
+          size_t(2) * series_buf_doubles(K, max_jmax + 1, nc, exact)) *
+         sizeof(double);
 }
 
 size_t series_scratch_bytes(long long nrowslots) {
