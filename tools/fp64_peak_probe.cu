@@ -52,6 +52,30 @@ __global__ void dmma_kernel(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// the Gram kernel's shape: NACC independent m16n8k4 accumulators per warp
+// (zk_gram.cu: a 64x32 warp tile = 16), fragments from registers
+template <int NACC>
+__global__ void dmma_tile_kernel(double* out, int iters) {
+  double acc[NACC][4];
+  for (int r = 0; r < NACC; ++r)
+    for (int i = 0; i < 4; ++i) acc[r][i] = 0;
+  double a[2], b[1];
+  a[0] = 1e-3 * threadIdx.x;
+  a[1] = 2e-3 * threadIdx.x;
+  b[0] = 1e-3 * (threadIdx.x + 1);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < NACC; ++r)
+      asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                   : "+d"(acc[r][0]), "+d"(acc[r][1]), "+d"(acc[r][2]), "+d"(acc[r][3])
+                   : "d"(a[0]), "d"(a[1]), "d"(b[0]));
+  }
+  double s = 0;
+  for (int r = 0; r < NACC; ++r)
+    for (int i = 0; i < 4; ++i) s += acc[r][i];
+  if (s == 12345.678) out[0] = s;
+}
+
 int main() {
   double* out;
   cudaMalloc(&out, 8);
@@ -95,6 +119,25 @@ int main() {
       double flops = fl[shape] * 4 * (iters / 4) * (double)sms * 4 * warps;
       printf("DMMA %-9s %2d warps/CTA x 4 CTA/SM: %.2f TFLOP/s (%s)\n", names[shape], warps,
              flops / best / 1e9, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  // occupancy sweep at the Gram kernel's warp tile (16 accumulators per warp)
+  for (int ctas : {1, 2, 4}) {
+    for (int warps : {4, 8, 16}) {
+      float best = 1e30f;
+      const int it16 = iters / 16;
+      for (int r = 0; r < 4; ++r) {
+        cudaEventRecord(e0);
+        dmma_tile_kernel<16><<<sms * ctas, warps * 32>>>(out, it16);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r && ms < best) best = ms;
+      }
+      double flops = fl[0] * 16 * (double)it16 * sms * ctas * warps;
+      printf("DMMA m16n8k4 x16 acc/warp %2d warps/CTA x %d CTA/SM (%2d warps/SM): %.2f TFLOP/s (%s)\n",
+             warps, ctas, warps * ctas, flops / best / 1e9, cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;
