@@ -12,6 +12,7 @@
 #include <sys/mman.h>
 #include <functional>
 #include <mutex>
+#include <memory>
 #include <new>
 #include <string>
 #include <thread>
@@ -61,6 +62,7 @@ class HostPool {
     cv_.notify_all();
     for (auto& t : workers_) t.join();
   }
+  size_t size() const { return workers_.size(); }
   // run fn(i) for i in [0, n) on the pool and the calling thread
   void parallel_for(int64_t n, const std::function<void(int64_t)>& fn) {
     {
@@ -177,11 +179,26 @@ int ensure_unique_view(zk_plan* plan) {
     }
     v.runs.push_back({slot_of[c], c, 1});
   }
+  // sent slot -> every output column it serves (CSR), for the staged path
+  const int64_t S = static_cast<int64_t>(kn.size());
+  v.dptr.assign(size_t(S) + 1, 0);
+  for (int64_t c = 0; c < M; ++c) v.dptr[size_t(v.slot[c]) + 1]++;
+  for (int64_t s = 0; s < S; ++s) v.dptr[size_t(s) + 1] += v.dptr[size_t(s)];
+  v.dcol.assign(size_t(M), 0);
+  {
+    std::vector<int64_t> fill(v.dptr.begin(), v.dptr.end() - 1);
+    for (int64_t c = 0; c < M; ++c) v.dcol[size_t(fill[size_t(v.slot[c])]++)] = c;
+  }
   int rc = zk_plan_create(plan->ctx, kn.data(), km.data(), static_cast<int64_t>(kn.size()),
                           h.max_order, &v.kplan);
   if (rc) return rc;
   v.built = true;
   return ZK_OK;
+}
+
+// output columns of a request evaluated through kplan (+ unique view)
+int64_t plan_M(const zk_plan* kplan, const zk_plan::UView* uv) {
+  return uv ? static_cast<int64_t>(uv->slot.size()) : kplan->host.M;
 }
 
 int ensure_chunk_events(zk_ctx* ctx, size_t n) {
@@ -335,6 +352,241 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
   return ZK_OK;
 }
 
+// Host output through a small page-locked staging ring (the default for the
+// radial basis with repeated keys and for pageable destinations).
+//
+// The kernel writes the plan's sent columns (one per unique (n,|m|) key when
+// uv != nullptr, every column otherwise) for a chunk of points into a dense
+// device image; the image crosses PCIe in batches of whole columns (~6 MB)
+// into a ring of R page-locked slots, and the host pool copies each landed
+// batch to every destination column it serves with non-temporal stores,
+// while the next batches are in flight. The ring is a few tens of MB, so it
+// stays in the host's last-level cache: host DRAM sees only the result's
+// streaming writes (4.12 GB at config 2), not the DMA write + read-back +
+// write of landing the unique columns in place and filling their +-m
+// partners from them (6.2 GB). Measured on the box (tools/e2e_stage_probe.cu,
+// config 2, pinned destination): 37.7 ms = the 2.08 GB PCIe transfer alone
+// (37.6 ms), vs 71-81 ms land-in-place + fill.
+int host_output_staged(zk_ctx* ctx, const zk_plan* kplan, const zk_plan::UView* uv,
+                       const double* rho, const double* theta, bool ang, int64_t P, int k,
+                       bool all, double* out, int64_t ld, int64_t ostride, bool scalar,
+                       bool host_in, bool pinned) {
+  const int NO = all ? k + 1 : 1;
+  const int64_t Mk = kplan->host.M;
+  const int nin = ang ? 2 : 1;
+  // output columns served by device column s: CSR over the sent slots
+  const std::vector<int64_t>* dptr = uv ? &uv->dptr : nullptr;
+  const std::vector<int64_t>* dcol = uv ? &uv->dcol : nullptr;
+  // device image: all points at once when it fits the budget, else point chunks
+  const size_t per_point = size_t(8) * size_t(Mk) * NO;
+  const size_t budget = size_t(std::max(64, env_int("ZK_IMAGE_MB", 4096))) << 20;
+  int64_t pc = static_cast<int64_t>(budget / per_point);
+  pc = std::max<int64_t>(1024, pc / 1024 * 1024);
+  pc = std::min<int64_t>(pc, P);
+  const int64_t nchunks = (P + pc - 1) / pc;
+  const int nimg = nchunks > 1 ? 2 : 1;
+  const size_t img_bytes = align_up(size_t(pc) * per_point, 256);
+  const size_t in_bytes = align_up(size_t(pc) * 8, 256);
+  for (int s = 0; s < nimg; ++s) {
+    int rc = ensure_scratch(ctx, s, img_bytes + in_bytes * nin);
+    if (rc) return rc;
+  }
+  // ring of R slots of ~ZK_RING_MB each, whole columns per batch
+  // 6 x 6 MB measured best of 4..12 slots x 2..8 MB (tools/e2e_sweep.py):
+  // smaller batches pay per-copy overheads, a larger ring spills out of LLC
+  const int R = std::max(2, env_int("ZK_RING_SLOTS", 6));
+  const size_t slot_target = size_t(std::max(1, env_int("ZK_RING_MB", 6))) << 20;
+  const int64_t col_bytes = pc * 8;
+  const int64_t B = std::max<int64_t>(1, static_cast<int64_t>(slot_target) / col_bytes);
+  const size_t slot_bytes = align_up(size_t(B) * size_t(col_bytes), 4096);
+  if (ctx->ring_bytes < slot_bytes * R) {
+    if (ctx->ring) {
+      ZK_CUDA(cudaStreamSynchronize(ctx->pipe[1]));
+      cudaFreeHost(ctx->ring);
+    }
+    ctx->ring = nullptr;
+    ctx->ring_bytes = 0;
+    cudaError_t e = cudaHostAlloc(&ctx->ring, slot_bytes * R, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ZK_ENOMEM, std::string("pinned staging ring: ") + cudaGetErrorString(e));
+    }
+    ctx->ring_bytes = slot_bytes * R;
+  }
+  while (ctx->ring_ev.size() < size_t(R)) {
+    cudaEvent_t e;
+    ZK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
+    ctx->ring_ev.push_back(e);
+  }
+  if (!ctx->pool) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    ctx->pool = new HostPool(static_cast<unsigned>(std::max(
+        0, env_int("ZK_HOST_THREADS", static_cast<int>(std::min(16u, hw))) - 1)));
+  }
+  if (!pinned && env_int("ZK_HUGEPAGE", 1)) {
+    // a fresh numpy result is untouched anonymous memory: transparent huge
+    // pages make the first-touch page faults 512x fewer
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(out);
+    const uintptr_t hi = lo + size_t((NO - 1) * ostride + ld * plan_M(kplan, uv)) * 8;
+    const uintptr_t pg = 4096;
+    const uintptr_t a = (lo + pg - 1) & ~(pg - 1), b = hi & ~(pg - 1);
+    if (b > a) madvise(reinterpret_cast<void*>(a), b - a, MADV_HUGEPAGE);
+  }
+  cudaStream_t cst = ctx->pipe[0], xst = ctx->pipe[1];  // compute, copy
+  // everything starts after work already queued on the launch stream
+  ZK_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
+  ZK_CUDA(cudaStreamWaitEvent(cst, ctx->ev_start, 0));
+  ZK_CUDA(cudaStreamWaitEvent(xst, ctx->ev_start, 0));
+  // ev_done[s]: "image s fully copied out" (recorded on the copy stream after
+  // a chunk's last batch); img_ready[s]: "image s computed" (compute stream)
+  cudaEvent_t img_ready[2] = {ctx->ev_img[0], ctx->ev_img[1]};
+  auto launch_chunk = [&](int64_t c) -> int {
+    const int s = static_cast<int>(c % nimg);
+    const int64_t p0 = c * pc, n = std::min<int64_t>(pc, P - p0);
+    char* base = static_cast<char*>(ctx->scratch[s]);
+    double* img = reinterpret_cast<double*>(base);
+    const double* r_in = rho + p0;
+    const double* t_in = ang ? theta + p0 : nullptr;
+    if (c >= nimg) ZK_CUDA(cudaStreamWaitEvent(cst, ctx->ev_done[s], 0));  // image free again
+    if (host_in) {
+      double* din = reinterpret_cast<double*>(base + img_bytes);
+      ZK_CUDA(cudaMemcpyAsync(din, rho + p0, size_t(n) * 8, cudaMemcpyHostToDevice, cst));
+      r_in = din;
+      if (ang) {
+        ZK_CUDA(cudaMemcpyAsync(din + in_bytes / 8, theta + p0, size_t(n) * 8,
+                                cudaMemcpyHostToDevice, cst));
+        t_in = din + in_bytes / 8;
+      }
+    }
+    int rc = launch_device(ctx, kplan, r_in, t_in, n, k, all, img, n, n * Mk, scalar, cst);
+    if (rc) return rc;
+    ZK_CUDA(cudaEventRecord(img_ready[s], cst));
+    return ZK_OK;
+  };
+  // batches: (chunk, order, first column), in that order
+  const int64_t nb_o = (Mk + B - 1) / B;
+  const int64_t per_chunk_batches = int64_t(NO) * nb_o;
+  const int64_t nbatches = nchunks * per_chunk_batches;
+  struct Batch {
+    int64_t c, s0, ns, n, p0;
+    int o;
+  };
+  auto batch_of = [&](int64_t b) {
+    Batch t{};
+    t.c = b / per_chunk_batches;
+    const int64_t r = b - t.c * per_chunk_batches;
+    t.o = static_cast<int>(r / nb_o);
+    t.s0 = (r - int64_t(t.o) * nb_o) * B;
+    t.ns = std::min<int64_t>(B, Mk - t.s0);
+    t.p0 = t.c * pc;
+    t.n = std::min<int64_t>(pc, P - t.p0);
+    return t;
+  };
+  int64_t launched = 0;  // chunks whose kernel is queued
+  auto enqueue = [&](int64_t b) -> int {
+    const Batch t = batch_of(b);
+    while (launched <= t.c && launched < nchunks) {
+      int rc = launch_chunk(launched++);
+      if (rc) return rc;
+    }
+    const int s = static_cast<int>(t.c % nimg);
+    if (b % per_chunk_batches == 0) ZK_CUDA(cudaStreamWaitEvent(xst, img_ready[s], 0));
+    const double* img = static_cast<const double*>(ctx->scratch[s]);
+    char* slot = static_cast<char*>(ctx->ring) + size_t(b % R) * slot_bytes;
+    ZK_CUDA(cudaMemcpyAsync(slot, img + (int64_t(t.o) * Mk + t.s0) * t.n, size_t(t.ns) * t.n * 8,
+                            cudaMemcpyDeviceToHost, xst));
+    ZK_CUDA(cudaEventRecord(ctx->ring_ev[size_t(b % R)], xst));
+    // the chunk's image is free once its last batch has landed
+    if ((b + 1) % per_chunk_batches == 0) ZK_CUDA(cudaEventRecord(ctx->ev_done[s], xst));
+    return ZK_OK;
+  };
+  for (int64_t b = 0; b < std::min<int64_t>(R, nbatches); ++b) {
+    int rc = enqueue(b);
+    if (rc) return rc;
+  }
+  // Streaming copy-out with no per-batch fork/join: one thread polls the
+  // ring events in order and publishes how many batches have landed; every
+  // pool thread claims (batch, column, row-segment) items in order and spins
+  // until its batch has landed; a slot goes back to the DMA queue once all
+  // its items are copied.
+  const int64_t seg = std::max<int64_t>(1, std::min<int64_t>(pc, P) / 16384);  // ~128 KB items
+  std::vector<int64_t> item0(size_t(nbatches) + 1, 0);
+  for (int64_t b = 0; b < nbatches; ++b) item0[size_t(b) + 1] = item0[size_t(b)] + batch_of(b).ns * seg;
+  const int64_t nitems = item0[size_t(nbatches)];
+  std::atomic<int64_t> landed{0}, next_item{0}, next_enq{std::min<int64_t>(R, nbatches)};
+  std::unique_ptr<std::atomic<int64_t>[]> left(new std::atomic<int64_t>[size_t(nbatches)]);
+  for (int64_t b = 0; b < nbatches; ++b) left[size_t(b)] = item0[size_t(b) + 1] - item0[size_t(b)];
+  std::atomic<int> err{ZK_OK};
+  std::atomic<bool> poller_taken{false};
+  std::mutex enq_mu;
+  auto copy_item = [&](int64_t i) {
+    int64_t b = static_cast<int64_t>(std::upper_bound(item0.begin(), item0.end(), i) - item0.begin()) - 1;
+    const Batch t = batch_of(b);
+    const int64_t k = i - item0[size_t(b)];
+    const int64_t j = k / seg, g = k - j * seg;
+    const int64_t r0 = g * t.n / seg, r1 = (g + 1) * t.n / seg;
+    const int64_t s = t.s0 + j;
+    const double* slot = reinterpret_cast<const double*>(static_cast<char*>(ctx->ring) +
+                                                         size_t(b % R) * slot_bytes);
+    const double* src = slot + j * t.n + r0;
+    double* obase = out + int64_t(t.o) * ostride + t.p0 + r0;
+    if (dptr) {
+      for (int64_t q = (*dptr)[size_t(s)]; q < (*dptr)[size_t(s) + 1]; ++q)
+        column_copy(obase + (*dcol)[size_t(q)] * ld, src, size_t(r1 - r0));
+    } else {
+      column_copy(obase + s * ld, src, size_t(r1 - r0));
+    }
+    left[size_t(b)].fetch_sub(1, std::memory_order_acq_rel);
+  };
+  // requeue freed slots (any thread; serialized)
+  auto refill = [&]() {
+    std::unique_lock<std::mutex> l(enq_mu, std::try_to_lock);
+    if (!l.owns_lock()) return;
+    for (int64_t b = next_enq.load(); b < nbatches && left[size_t(b - R)].load() == 0; ++b) {
+      int rc = enqueue(b);
+      if (rc) {
+        err = rc;
+        landed = nbatches;  // unblock the copiers
+        return;
+      }
+      next_enq = b + 1;
+    }
+  };
+  const int nthreads = 1 + static_cast<int>(ctx->pool->size());
+  ctx->pool->parallel_for(nthreads, [&](int64_t) {
+    const bool poller = !poller_taken.exchange(true);
+    cudaSetDevice(ctx->device);  // refill() may enqueue copies from any thread
+    for (;;) {
+      if (poller) {  // publish every landed batch, in order
+        for (int64_t b = landed.load(); b < nbatches && b < next_enq.load(); ++b) {
+          if (cudaEventQuery(ctx->ring_ev[size_t(b % R)]) != cudaSuccess) break;
+          landed = b + 1;
+        }
+        refill();
+      }
+      const int64_t i = next_item.load();
+      if (i >= nitems) break;
+      const int64_t b = static_cast<int64_t>(std::upper_bound(item0.begin(), item0.end(), i) - item0.begin()) - 1;
+      if (b >= landed.load(std::memory_order_acquire)) {
+        if (poller) continue;
+        _mm_pause();
+        continue;
+      }
+      int64_t mine = i;
+      if (!next_item.compare_exchange_weak(mine, i + 1)) continue;
+      copy_item(i);
+      if (!poller && left[size_t(b)].load() == 0) refill();
+    }
+    if (poller) {  // queue whatever is left (nothing in the normal case)
+      while (next_enq.load() < nbatches && err.load() == ZK_OK) refill();
+    }
+  });
+  if (err.load() != ZK_OK) return err.load();
+  ZK_CUDA(cudaStreamSynchronize(cst));
+  ZK_CUDA(cudaStreamSynchronize(xst));
+  return ZK_OK;
+}
+
 int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const double* theta,
                 bool ang, int64_t P, int k, int all_orders, double* out, int64_t ld,
                 int64_t ostride, uint32_t flags) {
@@ -442,6 +694,9 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
   }
   const zk_plan* kplan = uniq ? uv->kplan : plan;  // what the kernel evaluates
   const int64_t Mk = kplan->host.M;                 // columns per chunk
+  if ((uniq || !pinned) && env_int("ZK_STAGED", 1) != 0)
+    return host_output_staged(ctx, kplan, uv, rho, theta, ang, P, k, all, out, ld, ostride,
+                              scalar, host_in, pinned);
   const size_t budget = size_t(env_int("ZK_CHUNK_MB", 256)) << 20;  // basis bytes per slot
   const size_t per_point = size_t(8) * size_t(Mk) * NO;
   int64_t pc = static_cast<int64_t>(budget / per_point);
@@ -632,6 +887,8 @@ int zk_ctx_create(int device, zk_ctx** out) {
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_switch, cudaEventDisableTiming);
   for (int s = 0; s < 2 && e == cudaSuccess; ++s)
     e = cudaEventCreateWithFlags(&ctx->ev_done[s], cudaEventDisableTiming | cudaEventBlockingSync);
+  for (int s = 0; s < 2 && e == cudaSuccess; ++s)
+    e = cudaEventCreateWithFlags(&ctx->ev_img[s], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     zk_ctx_destroy(ctx);
     return cuda_fail(e, "context creation");
@@ -656,8 +913,11 @@ int zk_ctx_destroy(zk_ctx* ctx) {
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
   if (ctx->ev_switch) cudaEventDestroy(ctx->ev_switch);
   if (ctx->comm_buf) cudaFree(ctx->comm_buf);
+  if (ctx->ring) cudaFreeHost(ctx->ring);
+  for (cudaEvent_t e : ctx->ring_ev) cudaEventDestroy(e);
   for (int s = 0; s < 2; ++s) {
     if (ctx->ev_done[s]) cudaEventDestroy(ctx->ev_done[s]);
+    if (ctx->ev_img[s]) cudaEventDestroy(ctx->ev_img[s]);
     if (ctx->hbounce[s]) cudaFreeHost(ctx->hbounce[s]);
   }
   for (cudaEvent_t e : ctx->chunk_ev) cudaEventDestroy(e);
@@ -706,6 +966,9 @@ int zk_ctx_release_buffers(zk_ctx* ctx) {
   if (ctx->comm_buf) cudaFree(ctx->comm_buf);
   ctx->comm_buf = nullptr;
   ctx->comm_bytes = 0;
+  if (ctx->ring) cudaFreeHost(ctx->ring);
+  ctx->ring = nullptr;
+  ctx->ring_bytes = 0;
   return ZK_OK;
 }
 

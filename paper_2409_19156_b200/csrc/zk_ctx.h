@@ -46,8 +46,13 @@ struct zk_ctx {
   void* hbounce[2] = {nullptr, nullptr};
   size_t hbounce_bytes[2] = {0, 0};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  cudaEvent_t ev_img[2] = {nullptr, nullptr};  // staged host output: image computed
   zk::HostPool* pool = nullptr;
   std::vector<cudaEvent_t> chunk_ev;  // per-chunk D2H completion (unique-column path)
+  // page-locked staging ring of the host-output path (host_output_staged)
+  void* ring = nullptr;
+  size_t ring_bytes = 0;
+  std::vector<cudaEvent_t> ring_ev;
   // K5 (normal-equation allreduce): packed [upper(G) | Bty] staging buffer
   void* comm_buf = nullptr;
   size_t comm_bytes = 0;
@@ -83,6 +88,7 @@ struct zk_plan {
     std::vector<int64_t> slot;                       // output column -> sent slot to copy
     std::vector<Run> runs;                           // contiguous sent-column runs
     std::vector<std::pair<int64_t, int64_t>> fill;   // (output column, source column)
+    std::vector<int64_t> dptr, dcol;                 // sent slot -> output columns (CSR)
     bool built = false;
   };
   UView uv;
