@@ -113,6 +113,17 @@ __device__ __forceinline__ double jacobi_step(const ChainCoef& c, double x, doub
   return __fma_rn(r, c.rcp_lead, q);
 }
 
+// The same step with mx = RN(mid_x x) precomputed (shared by the chains of
+// one degree, see radial_basis_body): identical rounding sequence.
+__device__ __forceinline__ double jacobi_step_mx(const ChainCoef& c, double mx, double p1,
+                                                 double p0) {
+  const double t = __dmul_rn(__dadd_rn(mx, c.mid_const), p1);
+  const double num = __dsub_rn(t, __dmul_rn(c.last, p0));
+  const double q = __dmul_rn(num, c.rcp_lead);
+  const double r = __fma_rn(-q, c.lead, num);
+  return __fma_rn(r, c.rcp_lead, q);
+}
+
 // Per-thread, j-independent factors of the assembly (zk/evaluate.py:124-149):
 // the rho powers and the integer prefactors that multiply them.
 template <int K>

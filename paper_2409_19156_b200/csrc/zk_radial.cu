@@ -394,30 +394,40 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
     // A holds the newest degree, B the one before.
     double(&A)[K + 1][VEC] = th.cur;
     double(&B)[K + 1][VEC] = th.prev;
+    // One step of all K+1 chains to degree j (chain i at jacobi degree j-i).
+    // Chain i has c = 2(j-i) + (alpha+i) + i = 2j + alpha, the same for every
+    // chain, so mid_x = (c-1)c(c-2) is shared: RN(mid_x u) is formed once per
+    // point and degree -- exactly the product each chain's step rounds
+    // (zk/evaluate.py:75), so the values are bitwise unchanged (k = 3: 3 of
+    // 42 FP64 ops per point and key saved).
+    auto step_all = [&](int jj, double(&dst)[K + 1][VEC], const double(&src)[K + 1][VEC]) {
+      double mx[VEC];
+      if constexpr (K > 0) {
+        const double mxc = coefp[jj].mid_x;  // chain 0 at degree jj
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) mx[v] = __dmul_rn(mxc, th.u[v]);
+      }
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        const ChainCoef c = load_coef(coefp + i * nj + (jj - i));
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          if constexpr (K > 0)
+            dst[i][v] = jacobi_step_mx(c, mx[v], src[i][v], dst[i][v]);
+          else
+            dst[i][v] = jacobi_step(c, th.u[v], src[i][v], dst[i][v]);
+        }
+      }
+    };
     int j = K + 2;
     for (; j + 1 <= jmax; j += 2) {
-#pragma unroll
-      for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = load_coef(coefp + i * nj + (j - i));
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) B[i][v] = jacobi_step(c, th.u[v], A[i][v], B[i][v]);
-      }
+      step_all(j, B, A);
       emit(j, B, std::true_type{}, std::integral_constant<int, K % 2>{});
-#pragma unroll
-      for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = load_coef(coefp + i * nj + (j + 1 - i));
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) A[i][v] = jacobi_step(c, th.u[v], B[i][v], A[i][v]);
-      }
+      step_all(j + 1, A, B);
       emit(j + 1, A, std::true_type{}, std::integral_constant<int, (K + 1) % 2>{});
     }
     if (j <= jmax) {
-#pragma unroll
-      for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = load_coef(coefp + i * nj + (j - i));
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) B[i][v] = jacobi_step(c, th.u[v], A[i][v], B[i][v]);
-      }
+      step_all(j, B, A);
       emit(j, B, std::true_type{}, std::integral_constant<int, K % 2>{});
     }
   }
