@@ -203,7 +203,8 @@ int zk_jacobi_chain(zk_ctx* ctx, const double* x, int64_t N, int j_max, int alph
  *   term_ptr[c+1]) in descending order, exact integers rounded once) times
  *   rho^low_exp[c]; an empty term range is the zero polynomial.
  * zk_ztt_eval     <- zk/evaluate.py:211-247 radial_ztt_table: the Zernike
- *   three-term recursion with rho^q seeds, columns (n, |m|), n <= 256.
+ *   three-term recursion with rho^q seeds, columns (n, |m|), any degree
+ *   (levels in registers to n = 256, in a device scratch table beyond).
  * out is column-major P x M (ld >= P). */
 int zk_direct_eval(zk_ctx* ctx, const double* rho, int64_t P, const double* coef,
                    const int32_t* term_ptr, const int32_t* low_exp, int64_t M, double* out,

@@ -71,6 +71,19 @@ from .tables import (
 
 __version__ = "0.1.0"
 
+
+def release_buffers() -> None:
+    """Give back host and device memory the library caches between calls: the
+    recycled numpy result buffers (hostpool) and every context's device
+    scratch, page-locked staging ring and bounce buffers
+    (zk_ctx_release_buffers). Everything is re-allocated on demand."""
+    from . import _lib, hostpool
+    hostpool.release()
+    with _lib._ctx_lock:
+        ctxs = list(_lib._contexts.values())
+    for ctx in ctxs:
+        ctx.release_buffers()
+
 __all__ = [
     "BatchRequest", "BoundViolation", "DedupPlan", "DegreeViolation", "EvalMatrix",
     "GridError", "MAX_DERIV_ORDER", "Mode", "ModeError", "ModeSet", "ParityViolation",
@@ -84,4 +97,5 @@ __all__ = [
     "solve_normal", "allreduce_normal_equations", "pack_normal_equations",
     "unpack_normal_equations", "shard_range", "radial_basis_shard",
     "radial_direct", "radial_direct_table", "radial_ztt", "radial_ztt_table",
+    "release_buffers",
 ]

@@ -55,25 +55,30 @@ direct_kernel(const double* __restrict__ rho, long long P, const double* __restr
 // One array L[m] holds, per index parity, the latest level: level n only
 // touches indices of n's parity, reading level n-1 (other parity) and level
 // n-2 (its own index, overwritten in place).
+// NMAX = 0: any degree, the level array lives in global memory (lg, [m][p],
+// point-fastest so every access is coalesced) -- the reference's memoised
+// recursion has no degree limit (zk/evaluate.py:211-241).
 template <int NMAX>
 __global__ void __launch_bounds__(128)
 ztt_kernel(const double* __restrict__ rho, long long P, int N,
            const int32_t* __restrict__ lvl_ptr, const int32_t* __restrict__ lvl_m,
-           const int32_t* __restrict__ lvl_col, double* __restrict__ out, long long ld) {
+           const int32_t* __restrict__ lvl_col, double* __restrict__ out, long long ld,
+           double* __restrict__ lg) {
   const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= P) return;
   const double r = rho[p];
-  double L[NMAX + 1];
+  double Lr[NMAX > 0 ? NMAX + 1 : 1];
+  auto L = [&](int m) -> double& { return NMAX > 0 ? Lr[m] : lg[m * P + p]; };
   for (int n = 0; n <= N; ++n) {
     for (int m = n & 1; m <= n; m += 2) {
       if (m == n) {
-        L[m] = dd_pow(r, n).hi;  // rho**n seed (zk/evaluate.py:229-230)
+        L(m) = dd_pow(r, n).hi;  // rho**n seed (zk/evaluate.py:229-230)
       } else {  // rho * (R_{n-1}^{|m-1|} + R_{n-1}^{m+1}) - R_{n-2}^m  (:232-234)
-        L[m] = __dsub_rn(__dmul_rn(r, __dadd_rn(L[m == 0 ? 1 : m - 1], L[m + 1])), L[m]);
+        L(m) = __dsub_rn(__dmul_rn(r, __dadd_rn(L(m == 0 ? 1 : m - 1), L(m + 1))), L(m));
       }
     }
     for (int t = __ldg(lvl_ptr + n); t < __ldg(lvl_ptr + n + 1); ++t)
-      out[static_cast<long long>(__ldg(lvl_col + t)) * ld + p] = L[__ldg(lvl_m + t)];
+      out[static_cast<long long>(__ldg(lvl_col + t)) * ld + p] = L(__ldg(lvl_m + t));
   }
 }
 
@@ -86,17 +91,19 @@ cudaError_t launch_direct(const double* rho, long long P, const double* coef,
   return cudaGetLastError();
 }
 
-int ztt_max_degree() { return 256; }
+int ztt_max_degree() { return 256; }  // register/local level array; beyond: global table
 
 cudaError_t launch_ztt(const double* rho, long long P, int N, const int32_t* lvl_ptr,
                        const int32_t* lvl_m, const int32_t* lvl_col, double* out, long long ld,
-                       cudaStream_t st) {
+                       double* levels, cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
   const unsigned grid = static_cast<unsigned>((P + 127) / 128);
   if (N <= 64)
-    ztt_kernel<64><<<grid, 128, 0, st>>>(rho, P, N, lvl_ptr, lvl_m, lvl_col, out, ld);
+    ztt_kernel<64><<<grid, 128, 0, st>>>(rho, P, N, lvl_ptr, lvl_m, lvl_col, out, ld, nullptr);
+  else if (N <= 256)
+    ztt_kernel<256><<<grid, 128, 0, st>>>(rho, P, N, lvl_ptr, lvl_m, lvl_col, out, ld, nullptr);
   else
-    ztt_kernel<256><<<grid, 128, 0, st>>>(rho, P, N, lvl_ptr, lvl_m, lvl_col, out, ld);
+    ztt_kernel<0><<<grid, 128, 0, st>>>(rho, P, N, lvl_ptr, lvl_m, lvl_col, out, ld, levels);
   return cudaGetLastError();
 }
 

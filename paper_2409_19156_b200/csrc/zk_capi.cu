@@ -1460,8 +1460,6 @@ int zk_ztt_eval(zk_ctx* ctx, const double* rho, int64_t P, const int32_t* mode_n
   if (!err.empty()) return fail(ZK_EINVAL, err);
   int N = 0;
   for (int64_t c = 0; c < M; ++c) N = std::max(N, mode_n[c]);
-  if (N > zk::ztt_max_degree())
-    return fail(ZK_EINVAL, "ztt baseline supports n <= " + std::to_string(zk::ztt_max_degree()));
   // per level n: the (|m|, column) pairs to emit, in column order
   std::vector<int32_t> ptr(static_cast<size_t>(N) + 2, 0);
   std::vector<int32_t> lm(static_cast<size_t>(M)), lc(static_cast<size_t>(M));
@@ -1476,16 +1474,19 @@ int zk_ztt_eval(zk_ctx* ctx, const double* rho, int64_t P, const int32_t* mode_n
   std::lock_guard<std::mutex> lock(ctx->mu);
   ZK_CUDA(cudaSetDevice(ctx->device));
   const size_t pb = align_up(ptr.size() * 4, 256), mb = align_up(size_t(M) * 4, 256);
+  // degrees beyond the register-array kernel keep their levels in global memory
+  const size_t lb = N > zk::ztt_max_degree() ? align_up(size_t(N + 1) * size_t(P) * 8, 256) : 0;
   Staged s{};
-  int rc = stage_baseline(ctx, rho, P, M, out, ld, flags, pb + 2 * mb, s);
+  int rc = stage_baseline(ctx, rho, P, M, out, ld, flags, pb + 2 * mb + lb, s);
   if (rc) return rc;
   int32_t* dptr = reinterpret_cast<int32_t*>(s.tail);
   int32_t* dm = reinterpret_cast<int32_t*>(s.tail + pb);
   int32_t* dc = reinterpret_cast<int32_t*>(s.tail + pb + mb);
+  double* dlev = lb ? reinterpret_cast<double*>(s.tail + pb + 2 * mb) : nullptr;
   ZK_CUDA(cudaMemcpyAsync(dptr, ptr.data(), ptr.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
   ZK_CUDA(cudaMemcpyAsync(dm, lm.data(), size_t(M) * 4, cudaMemcpyHostToDevice, ctx->stream));
   ZK_CUDA(cudaMemcpyAsync(dc, lc.data(), size_t(M) * 4, cudaMemcpyHostToDevice, ctx->stream));
-  ZK_CUDA(zk::launch_ztt(s.rho, P, N, dptr, dm, dc, s.out, s.ld, ctx->stream));
+  ZK_CUDA(zk::launch_ztt(s.rho, P, N, dptr, dm, dc, s.out, s.ld, dlev, ctx->stream));
   ctx->launches += 1;
   // the host tables above are copied asynchronously: finish before they go out of scope
   return finish_baseline(ctx, P, M, out, ld, flags, s);

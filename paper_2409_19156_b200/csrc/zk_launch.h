@@ -86,9 +86,10 @@ cudaError_t launch_direct(const double* rho, long long P, const double* coef,
                           const int32_t* term_ptr, const int32_t* low_exp, long long M,
                           double* out, long long ld, cudaStream_t st);
 int ztt_max_degree();
+// levels: (N+1) x P scratch doubles, used when N > ztt_max_degree()
 cudaError_t launch_ztt(const double* rho, long long P, int N, const int32_t* lvl_ptr,
                        const int32_t* lvl_m, const int32_t* lvl_col, double* out, long long ld,
-                       cudaStream_t st);
+                       double* levels, cudaStream_t st);
 
 cudaError_t launch_radial_dd(const GroupRec* groups, int ngroups, const int32_t* rowptr,
                              const int32_t* cols, const double* rho_hi, const double* rho_lo,

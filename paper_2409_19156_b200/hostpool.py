@@ -8,8 +8,13 @@ than the whole PCIe transfer (measured on the B200 box: 170 ms per
 per call). Large results are therefore carved from buffers that earlier
 results released: an array handed out by :func:`take` keeps its buffer alive
 through ``ndarray.base``; when the last view dies the buffer returns to a
-size-keyed free list (bounded by ``ZK_RESULT_POOL_MB``, default 8192; 0
-disables) and the next result of that size reuses its already-faulted pages.
+size-keyed free list and the next result of that size reuses its
+already-faulted pages. Bounds: by default the pool keeps ONE released buffer
+(the most recent, at most 8 GB) -- the repeated-request case it exists for,
+without surprising a drop-in caller with gigabytes of retained RSS after its
+results died; ``ZK_RESULT_POOL_MB=<n>`` keeps any number of buffers up to n
+MB in total, ``0`` disables the pool. ``release()`` (``release_buffers()`` at
+the package level) frees everything the pool holds.
 Values never depend on the pool -- every element of a result is written by
 the library before it is returned.
 
@@ -56,8 +61,9 @@ class _Lease:
 
 
 class ResultPool:
-    def __init__(self, cap_bytes: int):
+    def __init__(self, cap_bytes: int, max_buffers: int | None = None):
         self.cap = cap_bytes
+        self.max_buffers = max_buffers  # None: bounded by bytes only
         self.free: OrderedDict[int, list[np.ndarray]] = OrderedDict()
         self.held = 0
         self.lock = threading.RLock()  # re-entrant: a GC-triggered release may run inside take()
@@ -107,15 +113,22 @@ class ResultPool:
             self._unpin(buf)
             return
         with self.lock:
-            while self.held + nbytes > self.cap and self.free:
+            while self.free and (self.held + nbytes > self.cap or (
+                    self.max_buffers is not None and self.count() >= self.max_buffers)):
                 size, lst = next(iter(self.free.items()))  # least recently released size
                 self._unpin(lst.pop())
                 self.held -= size
                 if not lst:
                     del self.free[size]
+            if self.max_buffers == 0:
+                self._unpin(buf)
+                return
             self.free.setdefault(nbytes, []).append(buf)
             self.free.move_to_end(nbytes)
             self.held += nbytes
+
+    def count(self) -> int:
+        return sum(len(v) for v in self.free.values())
 
     def clear(self) -> None:
         with self.lock:
@@ -126,8 +139,20 @@ class ResultPool:
             self.held = 0
 
 
-POOL = ResultPool(int(os.environ.get("ZK_RESULT_POOL_MB", "8192")) << 20)
+def _default_pool() -> ResultPool:
+    mb = os.environ.get("ZK_RESULT_POOL_MB")
+    if mb is None:
+        return ResultPool(8192 << 20, max_buffers=1)
+    return ResultPool(int(mb) << 20)
+
+
+POOL = _default_pool()
 
 
 def take(count: int) -> np.ndarray:
     return POOL.take(count)
+
+
+def release() -> None:
+    """Free (and unlock) every buffer the result pool holds."""
+    POOL.clear()

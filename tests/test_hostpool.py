@@ -75,3 +75,23 @@ def test_pinning_failure_is_silent_without_a_device():
     gc.collect()
     pool.clear()
     assert not pool.pinned
+
+
+def test_default_pool_keeps_one_buffer_and_release_frees_it():
+    """Default bound (no ZK_RESULT_POOL_MB): the most recently released
+    buffer only; release() (package: release_buffers()) empties the pool."""
+    pool = hostpool.ResultPool(8192 << 20, max_buffers=1)
+    a, b, c = pool.take(3_000_000), pool.take(4_000_000), pool.take(5_000_000)
+    del a, b, c
+    gc.collect()
+    assert pool.count() == 1 and pool.held in (24_000_000, 32_000_000, 40_000_000)
+    pool.clear()
+    assert pool.count() == 0 and pool.held == 0
+    assert hostpool.POOL.max_buffers == 1  # the module default
+    import paper_2409_19156_b200 as zb
+    keep = hostpool.take(2_000_000)
+    del keep
+    gc.collect()
+    assert hostpool.POOL.count() == 1
+    zb.release_buffers()  # no contexts without a GPU: only the pool is emptied
+    assert hostpool.POOL.count() == 0 and hostpool.POOL.held == 0
