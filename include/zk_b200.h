@@ -68,6 +68,11 @@ extern "C" {
 #define ZK_HOST_OUTPUT  2u   /* out / f / G / Bty are host pointers           */
 #define ZK_ASYNC        4u   /* device-only call: do not synchronize on return */
 #define ZK_STORE_SCALAR 8u   /* force the scalar (8-byte) store path (testing)  */
+/* Every rho power correctly rounded at ANY rho (the exponent carried apart,
+ * subnormal powers rounded once). The default path is correctly rounded while
+ * rho^(|m|+k) >= ~2^-916 and within a few subnormal ulps below (values
+ * < ~1e-270); this mode costs one point per thread (also: env ZK_EXACT_POW=1). */
+#define ZK_EXACT_POW    16u
 
 #define ZK_MAX_DERIV_ORDER 3 /* zk/evaluate.py:19 */
 

@@ -290,14 +290,15 @@ Geometry geometry(const zk_ctx* ctx, const zk_plan* plan, int64_t P, int K, bool
 // One device-resident launch of K1/K2 over P points.
 int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const double* theta,
                   int64_t P, int K, bool all, double* out, int64_t ld, int64_t ostride,
-                  bool force_scalar, cudaStream_t st) {
+                  bool force_scalar, cudaStream_t st, bool exact_pow = false) {
   if (P == 0 || plan->host.groups.empty()) return ZK_OK;
   auto fits = [&](int v) {
     return (ld % v == 0) && (reinterpret_cast<uintptr_t>(out) % (8 * v) == 0) &&
            (!all || ostride % v == 0);
   };
+  exact_pow = exact_pow || env_int("ZK_EXACT_POW", 0) != 0;
   int vec = 1;
-  if (!force_scalar) {
+  if (!force_scalar && !exact_pow) {
     // 4 points per thread for the plain radial k=0 basis, 2 when the thread also
     // carries the angular factors or derivative chains (register budget)
     int want = env_int("ZK_VEC", (K == 0 && theta == nullptr) ? 4 : 2);
@@ -314,7 +315,7 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
       }
     }
   }
-  const bool tma = !force_scalar && vec >= 2 && env_int("ZK_TMA", 0) != 0;
+  const bool tma = !force_scalar && !exact_pow && vec >= 2 && env_int("ZK_TMA", 0) != 0;
   Geometry geo = geometry(ctx, plan, P, K, all, vec, tma);
   bool coef_global = false;
   if (geo.smem > ctx->max_smem) {
@@ -346,6 +347,7 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
   a.col_cap = geo.col_cap;
   a.stage_slots = geo.stage_slots;
   a.coef_global = coef_global ? 1 : 0;
+  a.exact_pow = exact_pow ? 1 : 0;
   cudaError_t e = zk::launch_radial(a, K, all, theta != nullptr, geo.vec, geo.tma, geo.grid, geo.smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "radial kernel launch");
   ctx->launches += 1;
@@ -370,7 +372,7 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
 int host_output_staged(zk_ctx* ctx, const zk_plan* kplan, const zk_plan::UView* uv,
                        const double* rho, const double* theta, bool ang, int64_t P, int k,
                        bool all, double* out, int64_t ld, int64_t ostride, bool scalar,
-                       bool host_in, bool pinned) {
+                       bool host_in, bool pinned, bool exactp) {
   const int NO = all ? k + 1 : 1;
   const int64_t Mk = kplan->host.M;
   const int nin = ang ? 2 : 1;
@@ -458,7 +460,7 @@ int host_output_staged(zk_ctx* ctx, const zk_plan* kplan, const zk_plan::UView* 
         t_in = din + in_bytes / 8;
       }
     }
-    int rc = launch_device(ctx, kplan, r_in, t_in, n, k, all, img, n, n * Mk, scalar, cst);
+    int rc = launch_device(ctx, kplan, r_in, t_in, n, k, all, img, n, n * Mk, scalar, cst, exactp);
     if (rc) return rc;
     ZK_CUDA(cudaEventRecord(img_ready[s], cst));
     return ZK_OK;
@@ -609,11 +611,12 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
   const bool host_in = (flags & ZK_HOST_INPUT) != 0;
   const bool host_out = (flags & ZK_HOST_OUTPUT) != 0;
   const bool scalar = (flags & ZK_STORE_SCALAR) != 0;
+  const bool exactp = (flags & ZK_EXACT_POW) != 0;
   const int nin = ang ? 2 : 1;
 
   if (!host_in && !host_out) {
     int rc = launch_device(ctx, plan, rho, ang ? theta : nullptr, P, k, all, out, ld, ostride,
-                           scalar, ctx->stream);
+                           scalar, ctx->stream, exactp);
     if (rc) return rc;
     if (!(flags & ZK_ASYNC)) ZK_CUDA(cudaStreamSynchronize(ctx->stream));
     return ZK_OK;
@@ -629,7 +632,7 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
     ZK_CUDA(cudaMemcpyAsync(drho, rho, size_t(P) * 8, cudaMemcpyHostToDevice, ctx->stream));
     if (ang)
       ZK_CUDA(cudaMemcpyAsync(dth, theta, size_t(P) * 8, cudaMemcpyHostToDevice, ctx->stream));
-    rc = launch_device(ctx, plan, drho, dth, P, k, all, out, ld, ostride, scalar, ctx->stream);
+    rc = launch_device(ctx, plan, drho, dth, P, k, all, out, ld, ostride, scalar, ctx->stream, exactp);
     if (rc) return rc;
     ZK_CUDA(cudaStreamSynchronize(ctx->stream));
     return ZK_OK;
@@ -668,7 +671,7 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
         t_in = din + in_bytes / 8;
       }
     }
-    rc = launch_device(ctx, plan, r_in, t_in, P, k, all, dbasis, P, P * M, scalar, ctx->stream);
+    rc = launch_device(ctx, plan, r_in, t_in, P, k, all, dbasis, P, P * M, scalar, ctx->stream, exactp);
     if (rc) return rc;
     ZK_CUDA(cudaMemcpyAsync(out, dbasis, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
     ZK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -696,7 +699,7 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
   const int64_t Mk = kplan->host.M;                 // columns per chunk
   if ((uniq || !pinned) && env_int("ZK_STAGED", 1) != 0)
     return host_output_staged(ctx, kplan, uv, rho, theta, ang, P, k, all, out, ld, ostride,
-                              scalar, host_in, pinned);
+                              scalar, host_in, pinned, exactp);
   const size_t budget = size_t(env_int("ZK_CHUNK_MB", 256)) << 20;  // basis bytes per slot
   const size_t per_point = size_t(8) * size_t(Mk) * NO;
   int64_t pc = static_cast<int64_t>(budget / per_point);
@@ -767,7 +770,7 @@ int eval_common(zk_ctx* ctx, const zk_plan* plan, const double* rho, const doubl
       }
     }
     const int64_t dld = pc;
-    int rc = launch_device(ctx, kplan, r_in, t_in, n, k, all, dbasis, dld, dld * Mk, scalar, st);
+    int rc = launch_device(ctx, kplan, r_in, t_in, n, k, all, dbasis, dld, dld * Mk, scalar, st, exactp);
     if (rc) return rc;
     if (bounce) {
       ZK_CUDA(cudaMemcpyAsync(ctx->hbounce[s], dbasis, size_t(dld) * Mk * NO * 8,

@@ -9,8 +9,10 @@
 // exhaustively for every lead with n <= 1000) -- i.e. bitwise
 // equal to the reference's IEEE `/ lead` at a third of the cost of a DDIV
 // sequence. rho**e is computed in double-double and rounded once (correctly
-// rounded up to ~2^-100 relative), the only place the kernels can differ from
-// numpy's SIMD pow (<= 0.67 ulp).
+// rounded up to ~2^-100 relative while the powers stay above ~2^-916; the
+// opt-in exact-power mode, make_powset_exact, carries the binary exponent
+// apart and is correctly rounded everywhere, subnormals included), the only
+// place the kernels can differ from numpy's SIMD pow (<= 0.67 ulp).
 #pragma once
 
 #include <cstdint>
@@ -204,6 +206,185 @@ __device__ __forceinline__ PowSet<K> make_powset_from(dd acc, double rho, int m)
 template <int K>
 __device__ __forceinline__ PowSet<K> make_powset(double rho, int m) {
   return make_powset_from<K>(dd_pow(rho, powset_base<K>(m)), rho, m);
+}
+
+// ---- rho powers with the binary exponent carried apart -------------------
+// rho = f 2^x (frexp, f in [0.5, 1)); f^e is powered in double-double with
+// the running value renormalised to [0.5, 1] after every product, so no
+// product's error term ever leaves the normal range, at any rho or degree.
+// The window's powers are then rounded once -- exactly (an exponent-field
+// add) when the result is normal, onto the 2^-1074 grid with ties-to-even
+// when it is subnormal. RN(rho^e) is therefore correct everywhere (up to the
+// double-double's ~2^-100 near-tie limit), including rho^(|m|+k) < 2^-916
+// where plain double-double powering loses its error terms.
+struct ddx {
+  double hi, lo;  // in [0.5, 1] x (1 + 2^-53)
+  int ex;         // value = (hi + lo) 2^ex
+};
+
+// x 2^k for normal x and a normal result (an exponent-field add, exact)
+__device__ __forceinline__ double scale2_exact(double x, int k) {
+  return x == 0.0 ? 0.0
+                  : __longlong_as_double(__double_as_longlong(x) +
+                                         (static_cast<long long>(k) << 52));
+}
+
+__device__ __forceinline__ void ddx_norm(ddx& a) {
+  if (a.hi < 0.5) {  // a product of two values in [0.5, 1]: one doubling at most
+    a.hi = __dmul_rn(a.hi, 2.0);
+    a.lo = __dmul_rn(a.lo, 2.0);
+    a.ex -= 1;
+  }
+}
+
+// (f 2^x)^e for f in [0.5, 1), e >= 0; left-to-right binary powering
+__device__ __forceinline__ ddx ddx_pow(double f, int x, int e) {
+  if (e <= 0) return ddx{1.0, 0.0, 0};
+  ddx r{f, 0.0, 0};
+  for (int bit = 30 - __clz(e); bit >= 0; --bit) {
+    const dd s = dd_sqr(dd{r.hi, r.lo});
+    r = ddx{s.hi, s.lo, 2 * r.ex};
+    ddx_norm(r);
+    if ((e >> bit) & 1) {
+      const dd t = dd_mul_d(dd{r.hi, r.lo}, f);
+      r.hi = t.hi;
+      r.lo = t.lo;
+      ddx_norm(r);
+    }
+  }
+  r.ex += x * e;
+  return r;
+}
+
+// a * (f 2^x), f the frexp mantissa of rho
+__device__ __forceinline__ ddx ddx_mul_f(ddx a, double f, int x) {
+  const dd t = dd_mul_d(dd{a.hi, a.lo}, f);
+  ddx r{t.hi, t.lo, a.ex + x};
+  ddx_norm(r);
+  return r;
+}
+
+// RN((hi + lo) 2^ex) onto the 2^-1074 grid, ties to even: the subnormal case
+// of ddx_round (a rare, divergent branch; inline -- an out-of-line call makes
+// every value live across it survive the call ABI: +30-50 registers)
+__device__ __forceinline__ double ddx_round_subnormal(double hi, double lo, int ex) {
+  const int s = ex + 1074;  // quanta: q = (hi + lo) 2^s, hi 2^s in [2^(s-1), 2^s]
+  if (s < 0) return 0.0;    // q < 0.5 (hi <= 1 + tiny): rounds to zero
+  const double qh = scale2_exact(hi, s), ql = scale2_exact(lo, s);  // exact, s <= 52
+  double n = floor(qh);
+  const double t = __dsub_rn(__dsub_rn(qh, n), 0.5);  // exact: frac(qh) - 1/2
+  const double d = __dadd_rn(t, ql);                   // sign of frac(q) - 1/2 (RN keeps it)
+  if (d > 0.0 || (d == 0.0 && (__double2ll_rz(n) & 1))) n += 1.0;
+  return __dmul_rn(n, 0x1p-1074);  // exact: n <= 2^52
+}
+
+__device__ __forceinline__ double ddx_round(const ddx& a) {
+  if (a.hi == 0.0) return 0.0;
+  // hi in [0.5, 1]: the result's binary exponent is ex - 1 (ex for hi == 1)
+  if (a.ex - 1 >= -1022) return scale2_exact(a.hi, a.ex);  // normal: hi is RN(hi + lo)
+  return ddx_round_subnormal(a.hi, a.lo, a.ex);
+}
+
+// PowSet from acc = rho^powset_base<K>(m) in double-double.
+// PowSet from the window w[t] = rho^(e_lo + t), t = 0..2K, e_lo = powset_base<K>(m)
+template <int K>
+__device__ __forceinline__ PowSet<K> make_powset_window(const double (&w)[2 * K + 1], int e_lo,
+                                                        int m) {
+  PowSet<K> s;
+  double p_m = 1.0, p_m1 = 1.0, p_m2 = 1.0, p_m3 = 1.0, p_p1 = 0.0, p_p2 = 0.0, p_p3 = 0.0;
+  if (m >= K) {
+    // common case (m is CTA-uniform): e_lo = m - K, the window maps to the
+    // named powers statically
+    p_m = w[K];
+    if constexpr (K >= 1) {
+      p_m1 = w[K - 1];
+      p_p1 = w[K + 1];
+    }
+    if constexpr (K >= 2) {
+      p_m2 = w[K - 2];
+      p_p2 = w[K + 2];
+    }
+    if constexpr (K >= 3) {
+      p_m3 = w[K - 3];
+      p_p3 = w[K + 3];
+    }
+  } else {
+    // m < K: exponents below zero clamp to rho^0 = 1 (zk/evaluate.py:116-117)
+    const int em1 = m - 1 > 0 ? m - 1 : 0;
+    const int em2 = m - 2 > 0 ? m - 2 : 0;
+    const int em3 = m - 3 > 0 ? m - 3 : 0;
+#pragma unroll
+    for (int t = 0; t <= 2 * K; ++t) {
+      const int e = e_lo + t;
+      const double v = w[t];
+      if (e == m) p_m = v;
+      if (e == em1) p_m1 = v;
+      if (e == em2) p_m2 = v;
+      if (e == em3) p_m3 = v;
+      if (e == m + 1) p_p1 = v;
+      if (e == m + 2) p_p2 = v;
+      if (e == m + 3) p_p3 = v;
+    }
+  }
+  const double md = static_cast<double>(m);
+  s.A0 = p_m;
+  s.A1 = __dmul_rn(md, p_m1);
+  s.B1 = p_p1;
+  s.A2 = __dmul_rn(static_cast<double>(static_cast<long long>(m - 1) * m), p_m2);
+  s.B2 = p_m;
+  s.C2 = p_p2;
+  s.A3 = __dmul_rn(static_cast<double>(static_cast<long long>(m - 2) * (m - 1) * m), p_m3);
+  s.B3 = p_m1;
+  s.C3 = p_p1;
+  s.D3 = p_p3;
+  return s;
+}
+
+// Does the window rho^(m-K) .. rho^(m+K) reach below 2^-900, where plain
+// double-double powering loses its error terms? (rho = f 2^x, rho < 2^x;
+// exact on the exponent field, conservative by at most one binade.)
+template <int K>
+__device__ __forceinline__ bool powset_needs_exact(double rho, int m) {
+  const long long b = __double_as_longlong(rho);
+  const int E = static_cast<int>((b >> 52) & 0x7ff);
+  if (rho == 0.0) return false;  // 0^e is exact
+  if (E == 0) return true;       // subnormal rho
+  return (E - 1023) * (powset_base<K>(m) + 2 * K) < -900;
+}
+
+// PowSet with every power RN(rho^e) (ddx powering, any rho and degree):
+// the window rho^(m-K) .. rho^(m+K), exponents below zero clamped to 0
+// (zk/evaluate.py:116-117, 0^0 = 1).
+template <int K>
+__device__ __forceinline__ PowSet<K> make_powset_exact(double rho, int m) {
+  const int e_lo = powset_base<K>(m);
+  double w[2 * K + 1];
+  if (rho == 0.0) {  // exact: 0^0 = 1, else 0
+#pragma unroll
+    for (int t = 0; t <= 2 * K; ++t) w[t] = (e_lo + t == 0) ? 1.0 : 0.0;
+  } else {
+    int x;
+    const double f = frexp(rho, &x);  // rho in [2^(x-1), 2^x)
+    if (!powset_needs_exact<K>(rho, m)) {
+      // every window power >= 2^-900: plain double-double powering keeps its
+      // error terms normal and .hi is already RN(rho^e) -- the common case,
+      // and the cheaper one (no renormalisation)
+      dd acc = dd_pow(rho, e_lo);
+#pragma unroll
+      for (int t = 0; t <= 2 * K; ++t) {
+        w[t] = acc.hi;
+        if (t < 2 * K) acc = dd_mul_d(acc, rho);
+      }
+    } else {
+      ddx acc = ddx_pow(f, x, e_lo);
+#pragma unroll
+      for (int t = 0; t <= 2 * K; ++t) {
+        w[t] = ddx_round(acc);
+        if (t < 2 * K) acc = ddx_mul_f(acc, f, x);
+      }
+    }
+  }
+  return make_powset_window<K>(w, e_lo, m);
 }
 
 // Radial value of order O from the chain values ch[i] = P_{j-i}^{(m+i,i)}(u),

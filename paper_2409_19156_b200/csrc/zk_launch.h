@@ -31,6 +31,8 @@ struct RadialArgs {
   int stage_slots;        // (column, order) slots per TMA staging stage
   int coef_global;        // 1: read the group's coefficient tables from global memory
                           //    (L1-cached broadcasts) instead of staging them in smem
+  int exact_pow;          // 1: every rho power correctly rounded at any rho (VEC = 1
+                          //    kernels, make_powset_exact; ZK_EXACT_POW)
 };
 
 int radial_stages(bool all);

@@ -165,7 +165,9 @@ struct Thread {
   }
 };
 
-template <int K, bool ALL, bool ANG, int VEC, bool TMA, bool GC = false>
+// EXACTP: the opt-in exact-power mode -- every rho power RN(rho^e) at any rho
+// (make_powset_exact: exponent carried apart, subnormal results rounded once)
+template <int K, bool ALL, bool ANG, int VEC, bool TMA, bool GC = false, bool EXACTP = false>
 __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
   using T = Thread<K, ALL, ANG, VEC>;
   constexpr int NO = T::NO;
@@ -277,7 +279,10 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
       for (int v = 0; v < VEC; ++v) {
         rho[v] = (p0 + v < a.P) ? __ldg(a.rho + p0 + v) : 0.0;
         th.u[v] = jacobi_u(rho[v]);
-        th.pw[v] = make_powset<K>(rho[v], alpha);
+        if constexpr (EXACTP)
+          th.pw[v] = make_powset_exact<K>(rho[v], alpha);
+        else
+          th.pw[v] = make_powset<K>(rho[v], alpha);
       }
       if constexpr (ANG) {
 #pragma unroll
@@ -445,6 +450,13 @@ radial_basis_kernel(const RadialArgs a) {
   radial_basis_body<K, ALL, ANG, VEC, TMA, GC>(a);
 }
 
+// the exact-power mode's kernels (one point per thread, direct stores)
+template <int K, bool ALL, bool ANG, bool GC>
+__global__ void __launch_bounds__(kRadialThreads)
+radial_basis_exact_kernel(const RadialArgs a) {
+  radial_basis_body<K, ALL, ANG, 1, false, GC, true>(a);
+}
+
 template <int K, bool ALL, bool ANG, int VEC, bool TMA>
 __global__ void __launch_bounds__(kRadialThreads + (TMA ? 32 : 0), 2)
 radial_basis_kernel_2cta(const RadialArgs a) {
@@ -505,6 +517,17 @@ static cudaError_t launch_v(const RadialArgs& a, int vec, bool tma, int grid, si
       return tma ? launch_t<K, ALL, ANG, 2, true>(a, grid, smem, st)
                  : launch_t<K, ALL, ANG, 2, false>(a, grid, smem, st);
     default:
+      if (a.exact_pow) {  // opt-in exact powers (launch_device forces VEC = 1)
+        void (*fn)(RadialArgs) = a.coef_global ? radial_basis_exact_kernel<K, ALL, ANG, true>
+                                               : radial_basis_exact_kernel<K, ALL, ANG, false>;
+        if (smem > 48 * 1024) {
+          cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+          if (e != cudaSuccess) return e;
+        }
+        fn<<<grid, kRadialThreads, smem, st>>>(a);
+        return cudaGetLastError();
+      }
       if (a.coef_global) {  // long-chain fallback (coefficients from global memory)
         void (*fn)(RadialArgs) = radial_basis_kernel<K, ALL, ANG, 1, false, true>;
         if (smem > 48 * 1024) {

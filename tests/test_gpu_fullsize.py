@@ -134,6 +134,28 @@ def test_config3_all_orders_sweep_bitwise_equal_to_single_orders(c2):
     torch.cuda.empty_cache()
 
 
+def test_config3_exact_power_mode_full_grid(c2, monkeypatch):
+    """The opt-in exact-power mode on the full C2 grid (k = 3, one sweep vs
+    one launch per order): bitwise equal everywhere, subnormal windows
+    included, and equal to the default mode wherever |value| >= 1e-250."""
+    modes, grid = c2
+    fast = device_basis(modes, grid, 3)
+    monkeypatch.setenv("ZK_EXACT_POW", "1")
+    mats = device_basis(modes, grid, 3, all_orders=True)
+    single = device_basis(modes, grid, 3)
+    assert torch.equal(mats[3], single)
+    m_abs = torch.tensor([abs(md.m) for md in modes], dtype=torch.float64, device="cuda")
+    lg = (m_abs[None, :] + 3) * torch.log2(torch.from_numpy(grid).cuda())[:, None]
+    normal = lg >= -916  # the default mode's powers are RN here (rho = 0: -inf*0 -> nan: exact too)
+    normal |= torch.isnan(lg)
+    assert torch.equal(single[normal], fast[normal])
+    idx = np.arange(0, P2, 1000)
+    sub = single[torch.from_numpy(idx).cuda()].cpu().numpy()
+    pts = np.ascontiguousarray(grid[idx])
+    ref = orc.radial_batch(pairs(modes), pts, 3, power=orc.cached_cr_power(pts))
+    assert np.array_equal(sub, ref, equal_nan=True)
+
+
 @pytest.fixture(scope="module")
 def c5():
     P = 1_000_000

@@ -450,6 +450,33 @@ def test_subnormal_rho_powers(k):
     assert (err <= 1e-13 + 1e-12 * np.abs(np.where(fin, want, 0.0))).all()
 
 
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_exact_power_mode_is_bitwise_everywhere(monkeypatch, k):
+    """The opt-in exact-power mode (ZK_EXACT_POW / the C-ABI flag
+    ZK_EXACT_POW): powers carried as (double-double mantissa, binary
+    exponent) and rounded once, subnormals included -- the reference
+    algorithm with correctly rounded powers reproduces EVERY entry bitwise,
+    also the ones test_subnormal_rho_powers exempts; above the bound the two
+    modes agree bit for bit."""
+    pairs_ = [(2008, -1876), (2281, -483), (2031, 1071), (1928, 1778), (2515, -703),
+              (400, 380), (600, 560), (40, 12), (100, 100), (100, 60)]
+    modes = zb.as_mode_set(pairs_)
+    pts = np.array([0.6810649396839922, 0.6629706704580528, 0.50270979, 0.82940846,
+                    0.02, 0.15, 0.3, 1e-160, 1e-5, 2e-5, 3e-300, 0.0])
+    fast = radial(modes, pts, k)
+    monkeypatch.setenv("ZK_EXACT_POW", "1")
+    got = radial(modes, pts, k)
+    want = orc.radial_batch([(md.n, md.m) for md in modes], pts, k, power=orc.cr_power)
+    assert np.array_equal(got, want, equal_nan=True)
+    from fractions import Fraction
+    normal = np.array([[float(Fraction(float(r)) ** (abs(md.m) + k)) >= 2.0 ** -916
+                        for md in modes] for r in pts])
+    assert np.array_equal(got[normal], fast[normal], equal_nan=True)
+    # the all-orders sweep in exact mode equals the single-order launches
+    mats = zb.evaluate_batch_all_orders(zb.BatchRequest(modes=modes, grid=pts, deriv_order=k))
+    assert np.array_equal(mats[k].values, got, equal_nan=True)
+
+
 @pytest.mark.parametrize("vec", ["4", "2", "1"])
 def test_store_paths_agree_bitwise(monkeypatch, vec):
     """Every store path (32/16/8-byte direct stores; the TMA bulk-store ring
