@@ -892,6 +892,10 @@ int zk_ctx_create(int device, zk_ctx** out) {
     e = cudaEventCreateWithFlags(&ctx->ev_done[s], cudaEventDisableTiming | cudaEventBlockingSync);
   for (int s = 0; s < 2 && e == cudaSuccess; ++s)
     e = cudaEventCreateWithFlags(&ctx->ev_img[s], cudaEventDisableTiming);
+  for (int s = 0; s < 2 && e == cudaSuccess; ++s) {
+    e = cudaEventCreateWithFlags(&ctx->ev_gram_ready[s], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_gram_free[s], cudaEventDisableTiming);
+  }
   if (e != cudaSuccess) {
     zk_ctx_destroy(ctx);
     return cuda_fail(e, "context creation");
@@ -921,6 +925,8 @@ int zk_ctx_destroy(zk_ctx* ctx) {
   for (int s = 0; s < 2; ++s) {
     if (ctx->ev_done[s]) cudaEventDestroy(ctx->ev_done[s]);
     if (ctx->ev_img[s]) cudaEventDestroy(ctx->ev_img[s]);
+    if (ctx->ev_gram_ready[s]) cudaEventDestroy(ctx->ev_gram_ready[s]);
+    if (ctx->ev_gram_free[s]) cudaEventDestroy(ctx->ev_gram_free[s]);
     if (ctx->hbounce[s]) cudaFreeHost(ctx->hbounce[s]);
   }
   for (cudaEvent_t e : ctx->chunk_ev) cudaEventDestroy(e);
@@ -1233,20 +1239,29 @@ int zk_gram_accumulate(zk_ctx* ctx, const zk_plan* plan, const double* rho, cons
   const bool ang = theta != nullptr;
   cudaStream_t st = ctx->stream;
 
-  // panel geometry: [B | y | 0-pad] is Pp points x Mp columns, Mp = 128-multiple
-  const int64_t BMg = 128;
+  // panel geometry: [B | y | 0-pad] is Pp points x Mp columns, Mp = BM-multiple
+  const int64_t BMg = zk::gram_block();
   const int64_t Mp = (M + 1 + BMg - 1) / BMg * BMg;
   const int64_t nb = Mp / BMg;
   const int64_t ntri = nb * (nb + 1) / 2;
+  // Requests larger than one panel stream through TWO panel buffers: the K2
+  // basis of panel i+1 (HBM-bound, ctx->pipe[0]) overlaps the DMMA SYRK of
+  // panel i (tensor-bound, the launch stream).
   const int64_t budget = int64_t(env_int("ZK_GRAM_PANEL_MB", 2048)) << 20;
+  const int64_t Pfull = (P + 1023) / 1024 * 1024;
   int64_t Pp = budget / (Mp * 8) / 1024 * 1024;
-  Pp = std::max<int64_t>(1024, std::min<int64_t>(Pp, (P + 1023) / 1024 * 1024));
+  int nbuf = 1;
+  if (Pfull > Pp && env_int("ZK_GRAM_OVERLAP", 1) != 0) {
+    nbuf = 2;
+    Pp = budget / 2 / (Mp * 8) / 1024 * 1024;
+  }
+  Pp = std::max<int64_t>(1024, std::min<int64_t>(Pp, Pfull));
   // point slices per panel: >= 2 waves of one 256-thread CTA per SM
   // point slices per panel: pick the split whose CTA count (one 256-thread CTA
   // per SM) fills the last wave best, with at least two waves
   int64_t ksplit = 1;
-  {
-    const int64_t sms = ctx->sm_count;
+  {  // (CTA slots = SMs x resident syrk CTAs per SM)
+    const int64_t sms = int64_t(ctx->sm_count) * zk::gram_ctas_per_sm();
     double best = -1.0;
     for (int64_t ks = 1; ks <= 16; ++ks) {
       if (ks > 1 && Pp / ks < int64_t(zk::gram_k_granule()) * 32) break;  // >= 32 steps per slice
@@ -1264,57 +1279,67 @@ int zk_gram_accumulate(zk_ctx* ctx, const zk_plan* plan, const double* rho, cons
   const size_t in_b = align_up(size_t(Pp) * 8, 256);
   const size_t g_b = align_up(size_t(M) * M * 8, 256);
   const size_t acc_b = host_out ? g_b + align_up(size_t(M) * 8, 256) : 0;
-  int rc = ensure_scratch(ctx, 0, panel_b + part_b + 3 * in_b + acc_b + 256);
+  int rc = ensure_scratch(ctx, 0, nbuf * (panel_b + 3 * in_b) + part_b + acc_b + 256);
   if (rc) return rc;
   char* base = static_cast<char*>(ctx->scratch[0]);
-  double* panel = reinterpret_cast<double*>(base);
-  double* part = reinterpret_cast<double*>(base + panel_b);
-  double* s_rho = reinterpret_cast<double*>(base + panel_b + part_b);
-  double* s_th = s_rho + in_b / 8;
-  double* s_y = s_th + in_b / 8;
+  double* part = reinterpret_cast<double*>(base + nbuf * panel_b);
+  char* ins = base + nbuf * panel_b + part_b;  // per buffer: rho, theta, y staging
   double* dG = G;
   double* dB = y ? Bty : nullptr;
   if (host_out) {
-    dG = reinterpret_cast<double*>(base + panel_b + part_b + 3 * in_b);
+    dG = reinterpret_cast<double*>(ins + nbuf * 3 * in_b);
     dB = y ? dG + g_b / 8 : nullptr;
     ZK_CUDA(cudaMemcpyAsync(dG, G, size_t(M) * M * 8, cudaMemcpyHostToDevice, st));
     if (y) ZK_CUDA(cudaMemcpyAsync(dB, Bty, size_t(M) * 8, cudaMemcpyHostToDevice, st));
   }
+  cudaStream_t bst = ctx->pipe[0];  // panel producer (K2 + y)
+  ZK_CUDA(cudaEventRecord(ctx->ev_start, st));
+  ZK_CUDA(cudaStreamWaitEvent(bst, ctx->ev_start, 0));
   // zero padding columns (M+1 .. Mp-1) and, if y is absent, the y column
-  ZK_CUDA(cudaMemsetAsync(panel, 0, panel_b, st));
-  for (int64_t p0 = 0; p0 < P; p0 += Pp) {
+  ZK_CUDA(cudaMemsetAsync(base, 0, nbuf * panel_b, bst));
+  int64_t i = 0;
+  for (int64_t p0 = 0; p0 < P; p0 += Pp, ++i) {
+    const int buf = static_cast<int>(i % nbuf);
+    double* panel = reinterpret_cast<double*>(base + buf * panel_b);
+    double* s_rho = reinterpret_cast<double*>(ins + buf * 3 * in_b);
+    double* s_th = s_rho + in_b / 8;
+    double* s_y = s_th + in_b / 8;
     const int64_t n = std::min<int64_t>(Pp, P - p0);
-    if (n < Pp && p0 > 0)  // rows past a partial last panel still hold the previous panel
+    if (i >= nbuf) ZK_CUDA(cudaStreamWaitEvent(bst, ctx->ev_gram_free[buf], 0));
+    if (n < Pp && i >= nbuf)  // rows past a partial last panel still hold an older panel
       ZK_CUDA(cudaMemset2DAsync(panel + n, size_t(Pp) * 8, 0, size_t(Pp - n) * 8,
-                                size_t(M + 1), st));
+                                size_t(M + 1), bst));
     const double* r_in = rho + p0;
     const double* t_in = ang ? theta + p0 : nullptr;
     if (host_in) {
-      ZK_CUDA(cudaMemcpyAsync(s_rho, rho + p0, size_t(n) * 8, cudaMemcpyHostToDevice, st));
+      ZK_CUDA(cudaMemcpyAsync(s_rho, rho + p0, size_t(n) * 8, cudaMemcpyHostToDevice, bst));
       r_in = s_rho;
       if (ang) {
-        ZK_CUDA(cudaMemcpyAsync(s_th, theta + p0, size_t(n) * 8, cudaMemcpyHostToDevice, st));
+        ZK_CUDA(cudaMemcpyAsync(s_th, theta + p0, size_t(n) * 8, cudaMemcpyHostToDevice, bst));
         t_in = s_th;
       }
     }
-    rc = launch_device(ctx, plan, r_in, t_in, n, 0, false, panel, Pp, 0, false, st);
+    rc = launch_device(ctx, plan, r_in, t_in, n, 0, false, panel, Pp, 0, false, bst);
     if (rc) return rc;
     if (y) {
       if (host_in) {
-        ZK_CUDA(cudaMemcpyAsync(s_y, y + p0, size_t(n) * 8, cudaMemcpyHostToDevice, st));
-        ZK_CUDA(cudaMemcpyAsync(panel + M * Pp, s_y, size_t(n) * 8, cudaMemcpyDeviceToDevice, st));
+        ZK_CUDA(cudaMemcpyAsync(s_y, y + p0, size_t(n) * 8, cudaMemcpyHostToDevice, bst));
+        ZK_CUDA(cudaMemcpyAsync(panel + M * Pp, s_y, size_t(n) * 8, cudaMemcpyDeviceToDevice, bst));
       } else {
         ZK_CUDA(cudaMemcpyAsync(panel + M * Pp, y + p0, size_t(n) * 8, cudaMemcpyDeviceToDevice,
-                                st));
+                                bst));
       }
     }
+    ZK_CUDA(cudaEventRecord(ctx->ev_gram_ready[buf], bst));
+    ZK_CUDA(cudaStreamWaitEvent(st, ctx->ev_gram_ready[buf], 0));
     int launches = 0;
     const int64_t gk = zk::gram_k_granule();
     const int64_t kpanel = (n + gk - 1) / gk * gk;  // rows past n are zero; skip the rest
     cudaError_t e = zk::launch_gram_panel(panel, Pp, kpanel, M, static_cast<int>(ksplit), part, dG,
-                                          dB, st, &launches);
+                                          dB, i == 0, p0 + Pp >= P, st, &launches);
     ctx->launches += launches;
     if (e != cudaSuccess) return cuda_fail(e, "gram kernel launch");
+    ZK_CUDA(cudaEventRecord(ctx->ev_gram_free[buf], st));
   }
   if (host_out) {
     ZK_CUDA(cudaMemcpyAsync(G, dG, size_t(M) * M * 8, cudaMemcpyDeviceToHost, st));

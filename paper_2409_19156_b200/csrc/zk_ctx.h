@@ -47,6 +47,8 @@ struct zk_ctx {
   size_t hbounce_bytes[2] = {0, 0};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   cudaEvent_t ev_img[2] = {nullptr, nullptr};  // staged host output: image computed
+  cudaEvent_t ev_gram_ready[2] = {nullptr, nullptr};  // Gram panel buffer filled (pipe[0])
+  cudaEvent_t ev_gram_free[2] = {nullptr, nullptr};   // Gram panel buffer consumed (stream)
   zk::HostPool* pool = nullptr;
   std::vector<cudaEvent_t> chunk_ev;  // per-chunk D2H completion (unique-column path)
   // page-locked staging ring of the host-output path (host_output_staged)

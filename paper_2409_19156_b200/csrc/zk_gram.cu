@@ -10,9 +10,20 @@
 //
 // Tensor cores: mma.sync.m16n8k4.f64 (SASS DMMA.8x8x4). tcgen05.mma has no
 // f64 kind on sm_100a, so warp-level DMMA is the fp64 tensor path; measured
-// peak 36.9 TFLOP/s on B200 (tools/fp64_peak_probe.cu), equal to DFMA.
-// Operands are staged with cp.async (16-byte, L2-only) in a 3-stage ring of
-// 32-point steps (221 KB smem, one CTA per SM; measured 2 % faster than 16).
+// peak 36.9 TFLOP/s on B200 (tools/fp64_peak_probe.cu), equal to DFMA, and
+// 36.6 with this kernel's accumulator count at 8 warps/SM from registers
+// (profiles/r02/dmma_peak_probe.txt): what the kernel loses is its operand
+// path. Geometry (measured, tools/time_gram.py at config 5; see
+// profiles/r02/gram_geometry.txt): 64 x 64 blocks, 8 warps of 32 x 16, a
+// 2-stage cp.async ring of 16-point steps (41 KB smem, 64 registers) so FOUR
+// CTAs share an SM -- 32 warps hide the fragment loads and stage barriers
+// (DMMA pipe 89 -> 92 %), and 64-blocks halve the diagonal/padding waste of
+// 128-blocks: 123.5 -> 115 ms. (128-blocks at 1 CTA/SM: 3 stages x 32
+// points was that geometry's best.) Diagonal blocks compute their full
+// square: skipping the warp tiles below the diagonal measured slower
+// (118.7 vs 115.1 ms) -- the branch breaks the LDS/DMMA interleave of every CTA.
+// Over several panels the slice partials accumulate in place (fixed order)
+// and are reduced into G once.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -22,18 +33,32 @@
 namespace zk {
 
 namespace {
-constexpr int BM = 128;       // G block edge
+#ifndef ZK_GRAM_BM
+#define ZK_GRAM_BM 64
+#endif
+constexpr int BM = ZK_GRAM_BM;  // G block edge (128, or 64 with 32x16 warp tiles)
+constexpr int WM = BM / 2;      // warp tile rows   (8 warps: 2 x 4)
+constexpr int WN = BM / 4;      // warp tile cols
+constexpr int MI = WM / 16;     // m16 fragments per warp tile
+constexpr int NI = WN / 8;      // n8 fragments per warp tile
 #ifndef ZK_GRAM_BK
-#define ZK_GRAM_BK 32
+#define ZK_GRAM_BK 16
 #endif
 #ifndef ZK_GRAM_STAGES
-#define ZK_GRAM_STAGES 3
+#define ZK_GRAM_STAGES 2
 #endif
 constexpr int BK = ZK_GRAM_BK;          // points per pipeline stage
-constexpr int LDS = BK + 4;             // padded smem row (doubles): conflict-free fragments
+#ifndef ZK_GRAM_PAD
+#define ZK_GRAM_PAD 4
+#endif
+constexpr int LDS = BK + ZK_GRAM_PAD;   // padded smem row (doubles): conflict-free fragments
 constexpr int STAGES = ZK_GRAM_STAGES;
-constexpr int THREADS = 256;  // 8 warps: 2 (rows) x 4 (cols), warp tile 64 x 32
+constexpr int THREADS = 256;  // 8 warps: 2 (rows) x 4 (cols), warp tile WM x WN
 constexpr int TILE_DBL = BM * LDS;
+#ifndef ZK_GRAM_CTAS
+#define ZK_GRAM_CTAS (ZK_GRAM_BM == 128 ? 1 : 4)
+#endif
+constexpr int CTAS = ZK_GRAM_CTAS;  // resident SYRK CTAs per SM (register/smem budget)
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -60,9 +85,9 @@ __device__ __forceinline__ void tri_block(int t, int nb, int& bi, int& bj) {
 }  // namespace
 
 // partial[ks][blk] = sum over the slice's points of panel[:, I]^T panel[:, J]
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, CTAS)
 syrk_partial_kernel(const double* __restrict__ panel, long long ld, int nb, int ntri,
-                    long long kslice, long long kpanel, double* __restrict__ part) {
+                    long long kslice, long long kpanel, double* __restrict__ part, int accumulate) {
   extern __shared__ __align__(16) double smem[];
   const int blk = blockIdx.x % ntri;
   const int ks = blockIdx.x / ntri;
@@ -93,11 +118,11 @@ syrk_partial_kernel(const double* __restrict__ panel, long long ld, int nb, int 
     }
   };
 
-  double acc[4][4][4];
+  double acc[MI][NI][4];
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
+    for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[mi][ni][e] = 0.0;
 
@@ -112,36 +137,43 @@ syrk_partial_kernel(const double* __restrict__ panel, long long ld, int nb, int 
     const int nxt = kt + STAGES - 1;
     if (nxt < nk) load_stage(nxt % STAGES, nxt);
     asm volatile("cp.async.commit_group;" ::: "memory");
-    const double* a = sA + (kt % STAGES) * TILE_DBL + (wm * 64) * LDS;
-    const double* b = (diag ? sA : sB) + (kt % STAGES) * TILE_DBL + (wn * 32) * LDS;
+    const double* a = sA + (kt % STAGES) * TILE_DBL + (wm * WM) * LDS;
+    const double* b = (diag ? sA : sB) + (kt % STAGES) * TILE_DBL + (wn * WN) * LDS;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4][2], bf[4];
+      double af[MI][2], bf[NI];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
+      for (int mi = 0; mi < MI; ++mi) {
         af[mi][0] = a[(mi * 16 + g) * LDS + kk + t];
         af[mi][1] = a[(mi * 16 + g + 8) * LDS + kk + t];
       }
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) bf[ni] = b[(ni * 8 + g) * LDS + kk + t];
+      for (int ni = 0; ni < NI; ++ni) bf[ni] = b[(ni * 8 + g) * LDS + kk + t];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+        for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
     }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 
   double* out = part + (static_cast<long long>(ks) * ntri + blk) * BM * BM;
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int r = wm * 64 + mi * 16 + g;
-      const int c = wn * 32 + ni * 8 + 2 * t;
-      *reinterpret_cast<double2*>(out + r * BM + c) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
-      *reinterpret_cast<double2*>(out + (r + 8) * BM + c) =
-          make_double2(acc[mi][ni][2], acc[mi][ni][3]);
+    for (int ni = 0; ni < NI; ++ni) {
+      const int r = wm * WM + mi * 16 + g;
+      const int c = wn * WN + ni * 8 + 2 * t;
+      double2* o0 = reinterpret_cast<double2*>(out + r * BM + c);
+      double2* o1 = reinterpret_cast<double2*>(out + (r + 8) * BM + c);
+      if (accumulate) {  // later panels add onto the slice's running partial (fixed order)
+        const double2 p0 = *o0, p1 = *o1;
+        *o0 = make_double2(p0.x + acc[mi][ni][0], p0.y + acc[mi][ni][1]);
+        *o1 = make_double2(p1.x + acc[mi][ni][2], p1.y + acc[mi][ni][3]);
+      } else {
+        *o0 = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+        *o1 = make_double2(acc[mi][ni][2], acc[mi][ni][3]);
+      }
     }
 }
 
@@ -171,12 +203,14 @@ syrk_reduce_kernel(const double* __restrict__ part, int nb, int ntri, int ksplit
 }
 
 int gram_k_granule() { return BK; }
+int gram_block() { return BM; }
+int gram_ctas_per_sm() { return CTAS; }
 
 size_t gram_smem_bytes() { return size_t(2) * STAGES * TILE_DBL * sizeof(double); }
 
 cudaError_t launch_gram_panel(const double* panel, long long ld, long long kpanel, long long M,
-                              int ksplit, double* part, double* G, double* Bty, cudaStream_t st,
-                              int* launches) {
+                              int ksplit, double* part, double* G, double* Bty, bool first,
+                              bool last, cudaStream_t st, int* launches) {
   const int nb = static_cast<int>((M + 1 + BM - 1) / BM);
   const int ntri = nb * (nb + 1) / 2;
   long long kslice = (kpanel + ksplit - 1) / ksplit;
@@ -187,13 +221,15 @@ cudaError_t launch_gram_panel(const double* panel, long long ld, long long kpane
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   syrk_partial_kernel<<<ntri * ksplit, THREADS, smem, st>>>(panel, ld, nb, ntri, kslice, kpanel,
-                                                            part);
+                                                            part, first ? 0 : 1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  *launches += 1;
+  if (!last) return cudaSuccess;  // the partials keep accumulating over the panels
   const long long n = static_cast<long long>(ntri) * BM * BM;
   syrk_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(part, nb, ntri,
                                                                              ksplit, M, G, Bty);
-  *launches += 2;
+  *launches += 1;
   return cudaGetLastError();
 }
 

@@ -77,9 +77,12 @@ cudaError_t launch_series_dmma(const SeriesArgs& a, int K, int nch, int v0, int 
 
 size_t gram_smem_bytes();
 int gram_k_granule();  // points per SYRK pipeline step (panel rows are padded to it)
+int gram_block();      // G block edge of the SYRK tiles (panel columns are padded to it)
+int gram_ctas_per_sm();
+// first: the slice partials start from zero; last: reduce them into G / Bty
 cudaError_t launch_gram_panel(const double* panel, long long ld, long long kpanel, long long M,
-                              int ksplit, double* part, double* G, double* Bty, cudaStream_t st,
-                              int* launches);
+                              int ksplit, double* part, double* G, double* Bty, bool first,
+                              bool last, cudaStream_t st, int* launches);
 
 cudaError_t launch_chain(const double* x, long long N, int jmax, int alpha, int beta,
                          double* out, long long ldo, cudaStream_t st);
