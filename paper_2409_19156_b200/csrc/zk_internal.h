@@ -11,12 +11,15 @@ namespace zk {
 // zk/evaluate.py:70-74 held exactly as binary64 plus the correctly rounded
 // reciprocal of `lead` (used for an exact, Markstein-corrected division).
 // Six doubles so a warp-uniform entry is three 16-byte shared-memory loads.
+// Field order: the four a chain step needs besides mid_x come first (two
+// 16-byte loads); mid_x -- shared by the k+1 chains of one degree, loaded
+// once per degree by K1 -- sits in the third pair.
 struct alignas(16) ChainCoef {
-  double mid_x;      // (c-1) c (c-2)
   double mid_const;  // (c-1) (alpha^2 - beta^2)
   double last;       // 2 (j+alpha-1)(j+beta-1) c
   double rcp_lead;   // RN(1/lead)
   double lead;       // 2 j (c-j)(c-2)
+  double mid_x;      // (c-1) c (c-2)
   double pad;
 };
 static_assert(sizeof(ChainCoef) == 48, "ChainCoef layout");

@@ -72,12 +72,26 @@ __device__ __forceinline__ ChainCoef load_coef(const ChainCoef* p) {
   const double2* q = reinterpret_cast<const double2*>(p);
   const double2 a = q[0], b = q[1], c = q[2];
   ChainCoef r;
-  r.mid_x = a.x;
-  r.mid_const = a.y;
-  r.last = b.x;
-  r.rcp_lead = b.y;
-  r.lead = c.x;
+  r.mid_const = a.x;
+  r.last = a.y;
+  r.rcp_lead = b.x;
+  r.lead = b.y;
+  r.mid_x = c.x;
   r.pad = c.y;
+  return r;
+}
+
+// the record without mid_x (two LDS.128), for steps that share RN(mid_x x)
+__device__ __forceinline__ ChainCoef load_coef_nomx(const ChainCoef* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = q[0], b = q[1];
+  ChainCoef r;
+  r.mid_const = a.x;
+  r.last = a.y;
+  r.rcp_lead = b.x;
+  r.lead = b.y;
+  r.mid_x = 0.0;
+  r.pad = 0.0;
   return r;
 }
 

@@ -414,7 +414,8 @@ __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
       }
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const ChainCoef c = load_coef(coefp + i * nj + (jj - i));
+        const ChainCoef c = K > 0 ? load_coef_nomx(coefp + i * nj + (jj - i))
+                                  : load_coef(coefp + i * nj + (jj - i));
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
           if constexpr (K > 0)
