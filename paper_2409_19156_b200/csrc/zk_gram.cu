@@ -24,9 +24,13 @@
 // (118.7 vs 115.1 ms) -- the branch breaks the LDS/DMMA interleave of every CTA.
 // Over several panels the slice partials accumulate in place (fixed order)
 // and are reduced into G once.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <mutex>
 
 #include "zk_launch.h"
 
@@ -177,6 +181,189 @@ syrk_partial_kernel(const double* __restrict__ panel, long long ld, int nb, int 
     }
 }
 
+// ---- TMA operand path (the default; ZK_GRAM_TMA=0 selects the cp.async ring)
+// Same tiles and warp layout; each stage's two operand tiles (16 points x 64
+// columns, 8 KB each) arrive by ONE 2-D tensor copy apiece
+// (cp.async.bulk.tensor, SASS UTMALDG) issued by thread 0, with 128-byte
+// swizzle so the dense tile's fragment loads stay conflict-free, and stages
+// are handed over through mbarriers (full: transaction bytes; empty: one
+// arrival per warp, after a proxy fence) instead of CTA barriers. C5: 115.1
+// -> 111.6 ms, bitwise the cp.async path (2 stages; 3: 112.4, 4: 111.9,
+// 6: 113.4 ms).
+namespace {
+#ifndef ZK_GRAM_TSTAGES
+#define ZK_GRAM_TSTAGES 2
+#endif
+constexpr int TSTAGES = ZK_GRAM_TSTAGES;
+constexpr int TTILE = BM * 16;  // doubles per operand tile (64 columns x 16 points)
+static_assert(BK == 16 && BM == 64, "TMA variant: 64-column blocks of 16-point steps");
+
+__device__ __forceinline__ unsigned sm_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(unsigned long long* b, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mb_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n"
+      "}\n" ::"r"(sm_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(sm_addr(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(sm_addr(bar))
+      : "memory");
+}
+}  // namespace
+
+__global__ void __launch_bounds__(THREADS, CTAS)
+syrk_tma_kernel(const __grid_constant__ CUtensorMap tmap, int nb, int ntri, long long kslice,
+                long long kpanel, double* __restrict__ part, int accumulate) {
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  // 1024-byte aligned stage tiles (128B swizzle), then the mbarriers. The
+  // padding is computed on the shared-window address and applied as an offset
+  // into the shared array, so every fragment read stays an LDS: generic LD.E
+  // reads (what a uintptr_t round trip produces) are not ordered before the
+  // mbarrier arrive that hands the stage back to the TMA engine -- measured:
+  // the refill overwrote tiles still being read.
+  const unsigned sbase = sm_addr(tsm_raw);
+  double* tsm = reinterpret_cast<double*>(tsm_raw + (((sbase + 1023u) & ~1023u) - sbase));
+  double* sA = tsm;
+  double* sB = tsm + TSTAGES * TTILE;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(sB + TSTAGES * TTILE);
+  unsigned long long* empty = full + TSTAGES;
+  const int blk = blockIdx.x % ntri;
+  const int ks = blockIdx.x / ntri;
+  int bi, bj;
+  tri_block(blk, nb, bi, bj);
+  const bool diag = bi == bj;
+  const long long k0 = ks * kslice;
+  const long long k1 = min(kpanel, k0 + kslice);
+  const int nk = k0 < k1 ? static_cast<int>((k1 - k0) / BK) : 0;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+  const unsigned bytes = (diag ? 1u : 2u) * TTILE * 8u;
+  const CUtensorMap* map = &tmap;  // the __grid_constant__ parameter itself (not a copy)
+  auto issue = [sA, sB, full, map, k0, bi, bj, diag, bytes](int s, int kt) {
+    const int p = static_cast<int>(k0) + kt * BK;
+    mb_expect(full + s, bytes);
+    tma_load_2d(sA + s * TTILE, map, p, bi * BM, full + s);
+    if (!diag) tma_load_2d(sB + s * TTILE, map, p, bj * BM, full + s);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < TSTAGES; ++s) {
+      mb_init(full + s, 1);
+      mb_init(empty + s, THREADS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < TSTAGES && s < nk; ++s) issue(s, s);
+
+  double acc[MI][NI][4];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[mi][ni][e] = 0.0;
+
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % TSTAGES;
+    const unsigned par = (kt / TSTAGES) & 1;
+    mb_wait(full + s, par);
+    // element (column r, point p) of a tile: r*128 B + ((p/2 ^ r%8)*16 + (p%2)*8) B;
+    // every fragment row has r % 8 == g
+    const char* a = reinterpret_cast<const char*>(sA + s * TTILE) + (wm * WM + g) * 128;
+    const char* b = reinterpret_cast<const char*>((diag ? sA : sB) + s * TTILE) +
+                    (wn * WN + g) * 128;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      const int off = ((((kk >> 1) + (t >> 1)) ^ g) << 4) | ((t & 1) << 3);
+      double af[MI][2], bf[NI];
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) {
+        af[mi][0] = *reinterpret_cast<const double*>(a + (mi * 16) * 128 + off);
+        af[mi][1] = *reinterpret_cast<const double*>(a + (mi * 16 + 8) * 128 + off);
+      }
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni)
+        bf[ni] = *reinterpret_cast<const double*>(b + (ni * 8) * 128 + off);
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+    }
+    // Hand the stage back: the fragment reads were generic-proxy loads and the
+    // refill is an async-proxy (TMA) write, so each lane orders its reads
+    // before the hand-over with a proxy fence; the warp's arrive (release) then
+    // reaches the producer's wait (acquire). Without the fence the refill
+    // overwrote tiles whose loads were still in flight (measured, P >= 2e4).
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(empty + s)) : "memory");
+    if (tid == 0 && kt + TSTAGES < nk) {  // refill once every warp has read the stage
+      mb_wait(empty + s, par);
+      issue(s, kt + TSTAGES);
+    }
+    __syncwarp();  // warp 0 reconverges before its next mma.sync.aligned
+  }
+
+  double* out = part + (static_cast<long long>(ks) * ntri + blk) * BM * BM;
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) {
+      const int r = wm * WM + mi * 16 + g;
+      const int c = wn * WN + ni * 8 + 2 * t;
+      double2* o0 = reinterpret_cast<double2*>(out + r * BM + c);
+      double2* o1 = reinterpret_cast<double2*>(out + (r + 8) * BM + c);
+      if (accumulate) {
+        const double2 p0 = *o0, p1 = *o1;
+        *o0 = make_double2(p0.x + acc[mi][ni][0], p0.y + acc[mi][ni][1]);
+        *o1 = make_double2(p1.x + acc[mi][ni][2], p1.y + acc[mi][ni][3]);
+      } else {
+        *o0 = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+        *o1 = make_double2(acc[mi][ni][2], acc[mi][ni][3]);
+      }
+    }
+}
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    cudaGetLastError();
+  });
+  return fn;
+}
+}  // namespace
+
 // G[i,j] += sum_ks part (mirrored), Bty[i] += column M; fixed summation order.
 __global__ void __launch_bounds__(256)
 syrk_reduce_kernel(const double* __restrict__ part, int nb, int ntri, int ksplit, long long M,
@@ -220,8 +407,33 @@ cudaError_t launch_gram_panel(const double* panel, long long ld, long long kpane
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  syrk_partial_kernel<<<ntri * ksplit, THREADS, smem, st>>>(panel, ld, nb, ntri, kslice, kpanel,
-                                                            part, first ? 0 : 1);
+  static const bool use_tma = [] {  // ZK_GRAM_TMA=0: the cp.async operand ring
+    const char* v = std::getenv("ZK_GRAM_TMA");
+    return !(v && *v && std::atoi(v) == 0);
+  }();
+  PFN_cuTensorMapEncodeTiled_v12000 enc = use_tma ? tensor_map_encoder() : nullptr;
+  if (enc) {
+    // the panel as a 2-D tensor: dim 0 = points (contiguous, ld), dim 1 = columns
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld),
+                                static_cast<cuuint64_t>(nb) * BM};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+    const cuuint32_t box[2] = {BK, BM};
+    const cuuint32_t estr[2] = {1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(panel), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    const size_t tsmem = 1024 + size_t(2) * TSTAGES * TTILE * 8 + 2 * TSTAGES * 8;
+    e = cudaFuncSetAttribute(syrk_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(tsmem));
+    if (e != cudaSuccess) return e;
+    syrk_tma_kernel<<<ntri * ksplit, THREADS, tsmem, st>>>(map, nb, ntri, kslice, kpanel, part,
+                                                           first ? 0 : 1);
+  } else {
+    syrk_partial_kernel<<<ntri * ksplit, THREADS, smem, st>>>(panel, ld, nb, ntri, kslice,
+                                                              kpanel, part, first ? 0 : 1);
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   *launches += 1;
