@@ -190,3 +190,23 @@ def test_device_entry_points_reject_wrong_dtype_or_device():
         zb.series_device(modes, torch.ones(len(modes), dtype=torch.float64), torch.rand(10, dtype=torch.float64))
     with pytest.raises(TypeError):
         zb.gram_device(modes, rho32.double().cpu())
+
+
+def test_gram_tma_and_cpasync_operand_paths_bitwise(tmp_path):
+    """K4's two operand paths -- TMA tensor copies into swizzled tiles through
+    an mbarrier ring (default) and the cp.async ring (ZK_GRAM_TMA=0) -- give
+    the same bits: same tiles, same DMMA order. 150k points = three panels
+    (double-buffered, partials accumulated over panels). The switch is read
+    once per process, hence the subprocesses (tools/gram_save.py)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        out = tmp_path / f"g{flag}.npy"
+        env = dict(os.environ, ZK_GRAM_TMA=flag)
+        subprocess.run([sys.executable, os.path.join(root, "tools", "gram_save.py"), str(out),
+                        "150000"], check=True, env=env, cwd=root, timeout=600)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
