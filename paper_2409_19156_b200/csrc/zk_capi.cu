@@ -519,6 +519,7 @@ int host_output_staged(zk_ctx* ctx, const zk_plan* kplan, const zk_plan::UView* 
   std::unique_ptr<std::atomic<int64_t>[]> left(new std::atomic<int64_t>[size_t(nbatches)]);
   for (int64_t b = 0; b < nbatches; ++b) left[size_t(b)] = item0[size_t(b) + 1] - item0[size_t(b)];
   std::atomic<int> err{ZK_OK};
+  std::string err_msg;  // set under enq_mu: g_err is per thread
   std::atomic<bool> poller_taken{false};
   std::mutex enq_mu;
   auto copy_item = [&](int64_t i) {
@@ -545,10 +546,11 @@ int host_output_staged(zk_ctx* ctx, const zk_plan* kplan, const zk_plan::UView* 
     std::unique_lock<std::mutex> l(enq_mu, std::try_to_lock);
     if (!l.owns_lock()) return;
     for (int64_t b = next_enq.load(); b < nbatches && left[size_t(b - R)].load() == 0; ++b) {
-      int rc = enqueue(b);
+      int rc = enqueue(b);  // (called under enq_mu)
       if (rc) {
+        err_msg = g_err;  // enqueue's message lives in this thread's g_err
         err = rc;
-        landed = nbatches;  // unblock the copiers
+        next_item = nitems;  // every thread leaves the copy loop
         return;
       }
       next_enq = b + 1;
@@ -561,7 +563,17 @@ int host_output_staged(zk_ctx* ctx, const zk_plan* kplan, const zk_plan::UView* 
     for (;;) {
       if (poller) {  // publish every landed batch, in order
         for (int64_t b = landed.load(); b < nbatches && b < next_enq.load(); ++b) {
-          if (cudaEventQuery(ctx->ring_ev[size_t(b % R)]) != cudaSuccess) break;
+          const cudaError_t q = cudaEventQuery(ctx->ring_ev[size_t(b % R)]);
+          if (q == cudaErrorNotReady) break;
+          if (q != cudaSuccess) {  // a failed copy: stop (the call reports it)
+            {
+              std::lock_guard<std::mutex> l(enq_mu);
+              err_msg = std::string("staged host output: ") + cudaGetErrorString(q);
+            }
+            err = ZK_ECUDA;
+            next_item = nitems;
+            break;
+          }
           landed = b + 1;
         }
         refill();
@@ -583,7 +595,11 @@ int host_output_staged(zk_ctx* ctx, const zk_plan* kplan, const zk_plan::UView* 
       while (next_enq.load() < nbatches && err.load() == ZK_OK) refill();
     }
   });
-  if (err.load() != ZK_OK) return err.load();
+  if (err.load() != ZK_OK) {
+    cudaStreamSynchronize(cst);
+    cudaStreamSynchronize(xst);
+    return fail(err.load(), err_msg);
+  }
   ZK_CUDA(cudaStreamSynchronize(cst));
   ZK_CUDA(cudaStreamSynchronize(xst));
   return ZK_OK;
