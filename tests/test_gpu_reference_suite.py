@@ -38,6 +38,7 @@ def test_reference_suite_on_the_b200_path():
     # criterion 9 asserts that the CLI bench's wall time rises strictly with n
     # for calls of 40-80 us: timing-flaky on the stock CPU path as well
     # (SURVEY.md fact 1). A failure is re-run twice on its own before it counts.
+    rerun_passed = 0
     if TIMING_FLAKY in failed:
         for _ in range(2):
             again = subprocess.run(
@@ -46,9 +47,10 @@ def test_reference_suite_on_the_b200_path():
                 cwd=TESTS, env=env, capture_output=True, text=True, timeout=300)
             if again.returncode == 0:
                 failed.discard(TIMING_FLAKY)
+                rerun_passed = 1
                 break
     assert failed <= FAIL_BY_DESIGN, out[-4000:]
     m = re.search(r"B200 kernel launches during the reference suite: (\d+)", out)
     assert m and int(m.group(1)) > 1000, out[-2000:]  # the GPU path really ran
     passed = re.search(r"(\d+) passed", out)
-    assert passed and int(passed.group(1)) >= 157, out[-2000:]
+    assert passed and int(passed.group(1)) + rerun_passed >= 157, out[-2000:]
