@@ -314,9 +314,9 @@ int zk_comm_create(zk_ctx* ctx, const void* id, int nranks, int rank, zk_comm** 
   if (rc) return rc;
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof(uid));
+  ZK_CUDA(cudaSetDevice(ctx->device));
   zk_comm* c = new (std::nothrow) zk_comm();
   if (!c) return fail(ZK_ENOMEM, "comm allocation failed");
-  ZK_CUDA(cudaSetDevice(ctx->device));
   ncclResult_t r = nccl().CommInitRank(&c->comm, nranks, uid, rank);
   if (r != ncclSuccess) {
     delete c;

@@ -304,7 +304,7 @@ def pack_normal_equations(G, r=None):
     n = int(_lib.lib.zk_gram_packed_count(M))
     if G.is_cuda:
         _device_f64(("G", G), ("r", r))
-        Gc = G.t().contiguous().t() if not G.t().is_contiguous() else G  # column-major view
+        Gc = G.contiguous()  # symmetric: row- and column-major storage are the same matrix
         out = torch.empty(n, dtype=torch.float64, device=G.device)
         ctx = _torch_ctx(G, None)
         _lib.check(_lib.lib.zk_gram_pack(ctx.handle, Gc.data_ptr(),
