@@ -29,6 +29,8 @@
 #include <mutex>
 #include <thread>
 #include <vector>
+#include <sys/mman.h>
+#include <cstdlib>
 
 #define CK(x)                                                              \
   do {                                                                     \
@@ -143,8 +145,22 @@ int main(int argc, char** argv) {
   double *dev, *out;
   CK(cudaMalloc(&dev, size_t(8) * P * U));
   CK(cudaMemset(dev, 0x3f, size_t(8) * P * U));
-  CK(cudaHostAlloc(reinterpret_cast<void**>(&out), size_t(8) * P * M, cudaHostAllocPortable));
-  std::memset(out, 0, size_t(8) * P * M);
+  // ZK_PROBE_THP=1: the destination is 2 MB transparent-huge-page memory,
+  // page-locked with cudaHostRegister (else cudaHostAlloc's 4 KB pages)
+  const bool thp = getenv("ZK_PROBE_THP") && atoi(getenv("ZK_PROBE_THP"));
+  if (thp) {
+    const size_t bytes = (size_t(8) * P * M + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    madvise(p, bytes, MADV_HUGEPAGE);
+    out = static_cast<double*>(p);
+    std::memset(out, 0, size_t(8) * P * M);
+    CK(cudaHostRegister(out, bytes, cudaHostRegisterPortable));
+    std::printf("destination: THP + cudaHostRegister\n");
+  } else {
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&out), size_t(8) * P * M, cudaHostAllocPortable));
+    std::memset(out, 0, size_t(8) * P * M);
+    std::printf("destination: cudaHostAlloc\n");
+  }
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   const int threads_list[] = {8, 16};
