@@ -32,7 +32,8 @@
 // order already differs from B @ c, so bitwise reproduction of each basis
 // value buys nothing here. The plan carries the prescaled coefficients
 // a = mid_x/lead, b = mid_const/lead, c = last/lead (TolCoef, correctly
-// rounded quotients of the exact integers), and a chain step is P_j = fma(fma(a, x, b), P_{j-1}, -c P_{j-2})
+// rounded quotients of the exact integers), and a chain step is
+// P_j = fma(fma(a, x, b), P_{j-1}, -c P_{j-2})
 // -- 3 FP64 instructions instead of the exact path's 8 (no Markstein
 // division). For k = 0 the group's rho^|m| is constant over the group's
 // keys, so it multiplies the two group sums once instead of every value:
@@ -181,260 +182,260 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
   }
   const long long ntiles = (a.P + (kThreads * VEC) - 1) / (kThreads * VEC);
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-  const long long p0 = tile * (kThreads * VEC) + tid * VEC;
+    const long long p0 = tile * (kThreads * VEC) + tid * VEC;
 
-  // angular factors cos/sin(alpha theta) for the ascending groups: exact
-  // sincos(fl(alpha theta)) at an anchor, then rotations by theta for small
-  // alpha steps (<= 4 per group, <= 8 since the anchor: ~1e-15 relative,
-  // far inside the series tolerance); saves most of the per-group sincos
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) {
-    const bool live = p0 + v < a.P;
-    const double r = live ? __ldg(a.rho + p0 + v) : 0.0;
-    const double t = (ANG && live) ? __ldg(a.theta + p0 + v) : 0.0;
-    double c1 = 1.0, s1 = 0.0;
-    if (ANG) sincos(t, &s1, &c1);
-    pk(kRho, v) = r;
-    pk(kTh, v) = t;
-    pk(kPwHi, v) = 1.0;
-    pk(kPwLo, v) = 0.0;
-    pk(kC1, v) = c1;
-    pk(kS1, v) = s1;
-    pk(kCs, v) = 1.0;
-    pk(kSn, v) = 0.0;
-  }
-  int e_cur = 0;
-  int a_cur = -1, since = 0;
-  double acc[NC][VEC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c)
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) acc[c][v] = 0.0;
-
-  // stage group gi's coefficients, prefactors and row pointers into buffer b
-  auto stage = [&](int gi, int b) {
-    if constexpr (!STAGED) return;
-    const GroupRec g = a.groups[gi];
-    const int nj = g.jmax + 1;
-    double* base = smem + b * buf_doubles;
-    const int ncoef = (K + 1) * nj * CS;
-    if constexpr (TOL) {  // the plan's prescaled coefficients (TolCoef)
-      const double* tsrc = reinterpret_cast<const double*>(a.tol + g.coef_off);
-      for (int t = tid; t < ncoef; t += kThreads) cp_async8(base + t, tsrc + t);
-    } else {
-      const double* csrc = reinterpret_cast<const double*>(a.coef + g.coef_off);
-      for (int t = tid; t < ncoef; t += kThreads) cp_async8(base + t, csrc + t);
-    }
-    double* abase = base + ncoef;
-    if (K > 0) {
-      const double* asrc = reinterpret_cast<const double*>(a.asmc + g.asm_off);
-      for (int t = tid; t < nj * 8; t += kThreads) cp_async8(abase + t, asrc + t);
-    }
-    double* rbase = abase + (K > 0 ? nj * 8 : 0);
-    const double* rsrc = rowc + static_cast<long long>(g.row0) * 2 * NC;
-    for (int t = tid; t < nj * 2 * NC; t += kThreads) cp_async8(rbase + t, rsrc + t);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-
-  if constexpr (STAGED) stage(0, 0);
-  int r_toff = 0;  // resident: this group's TolCoef offset (doubles)
-  for (int gi = 0; gi < a.ngroups; ++gi) {
-    if constexpr (STAGED) {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      __syncthreads();  // buffer gi&1 ready; everyone is done with buffer (gi+1)&1
-      if (gi + 1 < a.ngroups) stage(gi + 1, (gi + 1) & 1);
-    }
-
-    const GroupRec g = a.groups[gi];
-    const int alpha = g.alpha;
-    const int jmax = g.jmax;
-    const int nj = jmax + 1;
-    const double* base = RES ? smem + r_toff : smem + (gi & 1) * buf_doubles;
-    r_toff += 4 * (K + 1) * nj;
-    const ChainCoef* s_coef =
-        GLB ? a.coef + g.coef_off : reinterpret_cast<const ChainCoef*>(base);
-    const AsmCoef* s_asm =
-        GLB ? a.asmc + g.asm_off
-            : RES ? reinterpret_cast<const AsmCoef*>(r_asm) + g.asm_off
-                  : reinterpret_cast<const AsmCoef*>(base + (K + 1) * nj * CS);
-    const double* s_rc = GLB ? rowc + static_cast<long long>(g.row0) * 2 * NC
-                         : RES ? r_rc + static_cast<long long>(g.row0) * 2 * NC
-                               : base + (K + 1) * nj * CS + (K > 0 ? nj * 8 : 0);
-    // chain step of chain i to degree d (exact or tolerance mode)
-    auto step_at = [&](int i, int d, double x, double p1, double p0) {
-      if constexpr (TOL) {
-        return jacobi_step_tol(load_tol(base + (i * nj + d) * 4), x, p1, p0);
-      } else {
-        return jacobi_step(load_coef(s_coef + i * nj + d), x, p1, p0);
-      }
-    };
-
-    // rho powers: advance the double-double accumulator to rho^base (alpha ascends)
-    const int e_lo = powset_base<K>(alpha);
-    PowSet<K> pw[VEC];
-    double u[VEC];
+    // angular factors cos/sin(alpha theta) for the ascending groups: exact
+    // sincos(fl(alpha theta)) at an anchor, then rotations by theta for small
+    // alpha steps (<= 4 per group, <= 8 since the anchor: ~1e-15 relative,
+    // far inside the series tolerance); saves most of the per-group sincos
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
-      const double r = pk(kRho, v);
-      u[v] = jacobi_u(r);
-      dd acc_p{pk(kPwHi, v), pk(kPwLo, v)};
-      if (e_lo == e_cur + 1)
-        acc_p = dd_mul_d(acc_p, r);
-      else if (e_lo > e_cur)
-        acc_p = dd_mul(acc_p, dd_pow(r, e_lo - e_cur));
-      pk(kPwHi, v) = acc_p.hi;
-      pk(kPwLo, v) = acc_p.lo;
-      // k = 0 tolerance mode: rho^|m| (= acc_p.hi) is read back at the group's end
-      if constexpr (!(TOL && K == 0)) pw[v] = make_powset_from<K>(acc_p, r, alpha);
+      const bool live = p0 + v < a.P;
+      const double r = live ? __ldg(a.rho + p0 + v) : 0.0;
+      const double t = (ANG && live) ? __ldg(a.theta + p0 + v) : 0.0;
+      double c1 = 1.0, s1 = 0.0;
+      if (ANG) sincos(t, &s1, &c1);
+      pk(kRho, v) = r;
+      pk(kTh, v) = t;
+      pk(kPwHi, v) = 1.0;
+      pk(kPwLo, v) = 0.0;
+      pk(kC1, v) = c1;
+      pk(kS1, v) = s1;
+      pk(kCs, v) = 1.0;
+      pk(kSn, v) = 0.0;
     }
-    e_cur = e_lo > e_cur ? e_lo : e_cur;
-    if constexpr (ANG) {
-      const int step = alpha - a_cur;  // CTA-uniform
-      if (a_cur >= 0 && step <= 4 && since + step <= 8) {
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          const double c1 = pk(kC1, v), s1 = pk(kS1, v);
-          double cs = pk(kCs, v), sn = pk(kSn, v);
-          for (int t = 0; t < step; ++t) {
-            const double c = fma(cs, c1, -sn * s1);
-            sn = fma(sn, c1, cs * s1);
-            cs = c;
-          }
-          pk(kCs, v) = cs;
-          pk(kSn, v) = sn;
-        }
-        since += step;
-      } else {
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          double cs, sn;
-          sincos(__dmul_rn(static_cast<double>(alpha), pk(kTh, v)), &sn, &cs);
-          pk(kCs, v) = cs;
-          pk(kSn, v) = sn;
-        }
-        since = 0;
-      }
-      a_cur = alpha;
-    }
-
-    // per-group sums: the angular factors are constant over a group, so they
-    // multiply the group's two partial sums once (2 FMAs per key instead of 3)
-    double gx[NC][VEC], gy[NC][VEC];
+    int e_cur = 0;
+    int a_cur = -1, since = 0;
+    double acc[NC][VEC];
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) gx[c][v] = gy[c][v] = 0.0;
-    // fold degree j's value into the running sums; STEADY: all chains >= 2
-    auto fold = [&](int j, const double(&chs)[K + 1][VEC], auto steady) {
-      AsmCoef ac;
-      if constexpr (K > 0) ac = load_asm(s_asm + j);
-      double val[VEC];
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        double ch[K + 1];
-#pragma unroll
-        for (int i = 0; i <= K; ++i)
-          ch[i] = (decltype(steady)::value || j - i >= 0) ? chs[i][v] : 0.0;
-        if constexpr (TOL && K == 0)
-          val[v] = ch[0];  // rho^|m| multiplies the group sums (below)
-        else if constexpr (TOL)
-          val[v] = assemble_tol<K>(pw[v], ac, ch);
-        else
-          val[v] = assemble<K, K>(pw[v], ac, ch);
+      for (int v = 0; v < VEC; ++v) acc[c][v] = 0.0;
+
+    // stage group gi's coefficients, prefactors and row pointers into buffer b
+    auto stage = [&](int gi, int b) {
+      if constexpr (!STAGED) return;
+      const GroupRec g = a.groups[gi];
+      const int nj = g.jmax + 1;
+      double* base = smem + b * buf_doubles;
+      const int ncoef = (K + 1) * nj * CS;
+      if constexpr (TOL) {  // the plan's prescaled coefficients (TolCoef)
+        const double* tsrc = reinterpret_cast<const double*>(a.tol + g.coef_off);
+        for (int t = tid; t < ncoef; t += kThreads) cp_async8(base + t, tsrc + t);
+      } else {
+        const double* csrc = reinterpret_cast<const double*>(a.coef + g.coef_off);
+        for (int t = tid; t < ncoef; t += kThreads) cp_async8(base + t, csrc + t);
       }
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const double2 cpn = *reinterpret_cast<const double2*>(s_rc + (j * NC + c) * 2);
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          gx[c][v] = fma(val[v], cpn.x, gx[c][v]);  // the group's cos(|m| theta) part
-          if (ANG) gy[c][v] = fma(val[v], cpn.y, gy[c][v]);  // its sin(|m| theta) part
-        }
+      double* abase = base + ncoef;
+      if (K > 0) {
+        const double* asrc = reinterpret_cast<const double*>(a.asmc + g.asm_off);
+        for (int t = tid; t < nj * 8; t += kThreads) cp_async8(abase + t, asrc + t);
       }
+      double* rbase = abase + (K > 0 ? nj * 8 : 0);
+      const double* rsrc = rowc + static_cast<long long>(g.row0) * 2 * NC;
+      for (int t = tid; t < nj * 2 * NC; t += kThreads) cp_async8(rbase + t, rsrc + t);
+      asm volatile("cp.async.commit_group;" ::: "memory");
     };
 
-    double A[K + 1][VEC], B[K + 1][VEC];  // A: newest degree, B: the one before
-#pragma unroll
-    for (int j = 0; j <= K + 1; ++j) {  // prologue degrees, d-branches resolved at compile time
-      if (j > jmax) break;
-#pragma unroll
-      for (int i = 0; i <= K; ++i) {
-        const int d = j - i;
-        if (d == 0) {
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) A[i][v] = 1.0;
-        } else if (d == 1) {
-          const double a1 = static_cast<double>(alpha + i + 1);
-          const double ab2 = static_cast<double>(alpha + 2 * i + 2);
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            B[i][v] = A[i][v];
-            A[i][v] = jacobi_p1(a1, ab2, u[v]);
-          }
-        } else if (d >= 2) {
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            const double nx = step_at(i, d, u[v], A[i][v], B[i][v]);
-            B[i][v] = A[i][v];
-            A[i][v] = nx;
-          }
+    if constexpr (STAGED) stage(0, 0);
+    int r_toff = 0;  // resident: this group's TolCoef offset (doubles)
+    for (int gi = 0; gi < a.ngroups; ++gi) {
+      if constexpr (STAGED) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();  // buffer gi&1 ready; everyone is done with buffer (gi+1)&1
+        if (gi + 1 < a.ngroups) stage(gi + 1, (gi + 1) & 1);
+      }
+
+      const GroupRec g = a.groups[gi];
+      const int alpha = g.alpha;
+      const int jmax = g.jmax;
+      const int nj = jmax + 1;
+      const double* base = RES ? smem + r_toff : smem + (gi & 1) * buf_doubles;
+      r_toff += 4 * (K + 1) * nj;
+      const ChainCoef* s_coef =
+          GLB ? a.coef + g.coef_off : reinterpret_cast<const ChainCoef*>(base);
+      const AsmCoef* s_asm =
+          GLB ? a.asmc + g.asm_off
+              : RES ? reinterpret_cast<const AsmCoef*>(r_asm) + g.asm_off
+                    : reinterpret_cast<const AsmCoef*>(base + (K + 1) * nj * CS);
+      const double* s_rc = GLB ? rowc + static_cast<long long>(g.row0) * 2 * NC
+                           : RES ? r_rc + static_cast<long long>(g.row0) * 2 * NC
+                                 : base + (K + 1) * nj * CS + (K > 0 ? nj * 8 : 0);
+      // chain step of chain i to degree d (exact or tolerance mode)
+      auto step_at = [&](int i, int d, double x, double p1, double p0) {
+        if constexpr (TOL) {
+          return jacobi_step_tol(load_tol(base + (i * nj + d) * 4), x, p1, p0);
+        } else {
+          return jacobi_step(load_coef(s_coef + i * nj + d), x, p1, p0);
         }
-      }
-      fold(j, A, std::false_type{});
-    }
-    int j = K + 2;
-    for (; j + 1 <= jmax; j += 2) {
-#pragma unroll
-      for (int i = 0; i <= K; ++i) {
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) B[i][v] = step_at(i, j - i, u[v], A[i][v], B[i][v]);
-      }
-      fold(j, B, std::true_type{});
-#pragma unroll
-      for (int i = 0; i <= K; ++i) {
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) A[i][v] = step_at(i, j + 1 - i, u[v], B[i][v], A[i][v]);
-      }
-      fold(j + 1, A, std::true_type{});
-    }
-    if (j <= jmax) {
-#pragma unroll
-      for (int i = 0; i <= K; ++i) {
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) B[i][v] = step_at(i, j - i, u[v], A[i][v], B[i][v]);
-      }
-      fold(j, B, std::true_type{});
-    }
-    if constexpr (TOL && K == 0) {
+      };
+
+      // rho powers: advance the double-double accumulator to rho^base (alpha ascends)
+      const int e_lo = powset_base<K>(alpha);
+      PowSet<K> pw[VEC];
+      double u[VEC];
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
-        const double a0 = pk(kPwHi, v);  // rho^|m|
+        const double r = pk(kRho, v);
+        u[v] = jacobi_u(r);
+        dd acc_p{pk(kPwHi, v), pk(kPwLo, v)};
+        if (e_lo == e_cur + 1)
+          acc_p = dd_mul_d(acc_p, r);
+        else if (e_lo > e_cur)
+          acc_p = dd_mul(acc_p, dd_pow(r, e_lo - e_cur));
+        pk(kPwHi, v) = acc_p.hi;
+        pk(kPwLo, v) = acc_p.lo;
+        // k = 0 tolerance mode: rho^|m| (= acc_p.hi) is read back at the group's end
+        if constexpr (!(TOL && K == 0)) pw[v] = make_powset_from<K>(acc_p, r, alpha);
+      }
+      e_cur = e_lo > e_cur ? e_lo : e_cur;
+      if constexpr (ANG) {
+        const int step = alpha - a_cur;  // CTA-uniform
+        if (a_cur >= 0 && step <= 4 && since + step <= 8) {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            const double c1 = pk(kC1, v), s1 = pk(kS1, v);
+            double cs = pk(kCs, v), sn = pk(kSn, v);
+            for (int t = 0; t < step; ++t) {
+              const double c = fma(cs, c1, -sn * s1);
+              sn = fma(sn, c1, cs * s1);
+              cs = c;
+            }
+            pk(kCs, v) = cs;
+            pk(kSn, v) = sn;
+          }
+          since += step;
+        } else {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            double cs, sn;
+            sincos(__dmul_rn(static_cast<double>(alpha), pk(kTh, v)), &sn, &cs);
+            pk(kCs, v) = cs;
+            pk(kSn, v) = sn;
+          }
+          since = 0;
+        }
+        a_cur = alpha;
+      }
+
+      // per-group sums: the angular factors are constant over a group, so they
+      // multiply the group's two partial sums once (2 FMAs per key instead of 3)
+      double gx[NC][VEC], gy[NC][VEC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) gx[c][v] = gy[c][v] = 0.0;
+      // fold degree j's value into the running sums; STEADY: all chains >= 2
+      auto fold = [&](int j, const double(&chs)[K + 1][VEC], auto steady) {
+        AsmCoef ac;
+        if constexpr (K > 0) ac = load_asm(s_asm + j);
+        double val[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          double ch[K + 1];
+#pragma unroll
+          for (int i = 0; i <= K; ++i)
+            ch[i] = (decltype(steady)::value || j - i >= 0) ? chs[i][v] : 0.0;
+          if constexpr (TOL && K == 0)
+            val[v] = ch[0];  // rho^|m| multiplies the group sums (below)
+          else if constexpr (TOL)
+            val[v] = assemble_tol<K>(pw[v], ac, ch);
+          else
+            val[v] = assemble<K, K>(pw[v], ac, ch);
+        }
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          gx[c][v] *= a0;
-          if (ANG) gy[c][v] *= a0;
+          const double2 cpn = *reinterpret_cast<const double2*>(s_rc + (j * NC + c) * 2);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            gx[c][v] = fma(val[v], cpn.x, gx[c][v]);  // the group's cos(|m| theta) part
+            if (ANG) gy[c][v] = fma(val[v], cpn.y, gy[c][v]);  // its sin(|m| theta) part
+          }
+        }
+      };
+
+      double A[K + 1][VEC], B[K + 1][VEC];  // A: newest degree, B: the one before
+#pragma unroll
+      for (int j = 0; j <= K + 1; ++j) {  // prologue degrees, d-branches resolved at compile time
+        if (j > jmax) break;
+#pragma unroll
+        for (int i = 0; i <= K; ++i) {
+          const int d = j - i;
+          if (d == 0) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) A[i][v] = 1.0;
+          } else if (d == 1) {
+            const double a1 = static_cast<double>(alpha + i + 1);
+            const double ab2 = static_cast<double>(alpha + 2 * i + 2);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              B[i][v] = A[i][v];
+              A[i][v] = jacobi_p1(a1, ab2, u[v]);
+            }
+          } else if (d >= 2) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              const double nx = step_at(i, d, u[v], A[i][v], B[i][v]);
+              B[i][v] = A[i][v];
+              A[i][v] = nx;
+            }
+          }
+        }
+        fold(j, A, std::false_type{});
+      }
+      int j = K + 2;
+      for (; j + 1 <= jmax; j += 2) {
+#pragma unroll
+        for (int i = 0; i <= K; ++i) {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) B[i][v] = step_at(i, j - i, u[v], A[i][v], B[i][v]);
+        }
+        fold(j, B, std::true_type{});
+#pragma unroll
+        for (int i = 0; i <= K; ++i) {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) A[i][v] = step_at(i, j + 1 - i, u[v], B[i][v], A[i][v]);
+        }
+        fold(j + 1, A, std::true_type{});
+      }
+      if (j <= jmax) {
+#pragma unroll
+        for (int i = 0; i <= K; ++i) {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) B[i][v] = step_at(i, j - i, u[v], A[i][v], B[i][v]);
+        }
+        fold(j, B, std::true_type{});
+      }
+      if constexpr (TOL && K == 0) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const double a0 = pk(kPwHi, v);  // rho^|m|
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            gx[c][v] *= a0;
+            if (ANG) gy[c][v] *= a0;
+          }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const double cs = ANG ? pk(kCs, v) : 1.0, sn = ANG ? pk(kSn, v) : 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (ANG) {
+            acc[c][v] = fma(gx[c][v], cs, acc[c][v]);
+            acc[c][v] = fma(gy[c][v], sn, acc[c][v]);
+          } else {
+            acc[c][v] += gx[c][v];
+          }
         }
       }
     }
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      const double cs = ANG ? pk(kCs, v) : 1.0, sn = ANG ? pk(kSn, v) : 0.0;
+    for (int c = 0; c < NC; ++c)
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        if (ANG) {
-          acc[c][v] = fma(gx[c][v], cs, acc[c][v]);
-          acc[c][v] = fma(gy[c][v], sn, acc[c][v]);
-        } else {
-          acc[c][v] += gx[c][v];
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < NC; ++c)
-#pragma unroll
-    for (int v = 0; v < VEC; ++v)
-      if (p0 + v < a.P) a.f[p0 + v + (v0 + c) * a.ldf] = acc[c][v];
+      for (int v = 0; v < VEC; ++v)
+        if (p0 + v < a.P) a.f[p0 + v + (v0 + c) * a.ldf] = acc[c][v];
   }  // tiles
 }
 
