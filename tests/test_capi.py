@@ -88,3 +88,21 @@ def test_no_device_fails_loudly():
         pytest.skip("a CUDA device is present")
     with pytest.raises(RuntimeError):
         _lib.Context(0)
+
+
+def test_k5_entry_points_validate_without_a_gpu():
+    """The K5 (normal-equation allreduce) entry points reject bad arguments
+    before touching a device; the packed count is M(M+1)/2 + M."""
+    import ctypes as ct
+    lib = _lib.lib
+    assert lib.zk_gram_packed_count(0) == 0 and lib.zk_gram_packed_count(-3) == 0
+    assert lib.zk_gram_packed_count(1891) == 1891 * 1892 // 2 + 1891
+    assert lib.zk_gram_pack(None, None, None, 4, None, 0) == _lib.ZK_EINVAL
+    assert lib.zk_gram_unpack(None, None, 4, None, None, 0) == _lib.ZK_EINVAL
+    arr = ct.c_void_p * 1
+    assert lib.zk_gram_allreduce(None, 1, None, None, 4, 0) == _lib.ZK_EINVAL
+    assert lib.zk_gram_allreduce(arr(None), 0, arr(None), None, 4, 0) == _lib.ZK_EINVAL
+    assert lib.zk_comm_create(None, None, 1, 0, None) == _lib.ZK_EINVAL
+    assert lib.zk_comm_info(None, None, None) == _lib.ZK_EINVAL
+    assert lib.zk_comm_destroy(None) == _lib.ZK_OK
+    assert lib.zk_gram_allreduce_comm(None, None, None, 4, 0) == _lib.ZK_EINVAL
