@@ -1225,7 +1225,9 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const do
     // several coefficient vectors make the series a dense contraction: DMMA path
     const int dm = env_int("ZK_SERIES_DMMA", -1);
     const int nch = zk::series_dmma_chunks(static_cast<int>(std::min<int64_t>(ncoef, 32)));
-    const bool dmma = (dm < 0 ? ncoef >= 8 : dm != 0) &&
+    // (measured at config 5: FMA folding 2.28 vs DMMA 2.44 ms at 8 vectors,
+    // 4.30 vs 3.64 at 16; tools/series_vectors.py)
+    const bool dmma = (dm < 0 ? ncoef > 8 : dm != 0) &&
                       zk::series_dmma_smem_bytes(deriv_order, plan->host.max_jmax, nch) <=
                           ctx->max_smem;
     cudaError_t e = zk::launch_series(a, deriv_order, plan->host.max_jmax, nrowslots,

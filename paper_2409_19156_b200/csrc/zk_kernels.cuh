@@ -429,4 +429,36 @@ __device__ __forceinline__ double assemble(const PowSet<K>& s, const AsmCoef& a,
   }
 }
 
+// ---- tolerance mode (the series kernels, zk_series*.cu) -----------------
+// the tolerance-mode chain step: P_j = (a x + b) P_{j-1} - c P_{j-2}
+__device__ __forceinline__ TolCoef load_tol(const double* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 x = q[0], y = q[1];
+  return TolCoef{x.x, x.y, y.x, 0.0};
+}
+
+__device__ __forceinline__ double jacobi_step_tol(const TolCoef& c, double x, double p1,
+                                                  double p0) {
+  return fma(fma(c.a, x, c.b), p1, -(c.c * p0));
+}
+
+// assembly of zk/evaluate.py:124-149 with FMA contraction (tolerance mode)
+template <int K>
+__device__ __forceinline__ double assemble_tol(const PowSet<K>& s, const AsmCoef& a,
+                                               const double* ch) {
+  if constexpr (K == 0) {
+    return s.A0 * ch[0];
+  } else if constexpr (K == 1) {
+    return fma(s.A1, ch[0], -(a.c11 * s.B1) * ch[1]);
+  } else if constexpr (K == 2) {
+    const double t = fma(-(a.c21 * s.B2), ch[1], s.A2 * ch[0]);
+    return fma(a.c22 * s.C2, ch[2], t);
+  } else {
+    double t = fma(-(a.c31 * s.B3), ch[1], s.A3 * ch[0]);
+    t = fma(a.c32 * s.C3, ch[2], t);
+    return fma(-(a.c33 * s.D3), ch[3], t);
+  }
+}
+
+
 }  // namespace zk

@@ -95,36 +95,6 @@ __global__ void series_rowsum_kernel(const GroupRec* __restrict__ groups,
   }
 }
 
-// the tolerance-mode chain step: P_j = (a x + b) P_{j-1} - c P_{j-2}
-__device__ __forceinline__ TolCoef load_tol(const double* p) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-  const double2 x = q[0], y = q[1];
-  return TolCoef{x.x, x.y, y.x, 0.0};
-}
-
-__device__ __forceinline__ double jacobi_step_tol(const TolCoef& c, double x, double p1,
-                                                  double p0) {
-  return fma(fma(c.a, x, c.b), p1, -(c.c * p0));
-}
-
-// assembly of zk/evaluate.py:124-149 with FMA contraction (tolerance mode)
-template <int K>
-__device__ __forceinline__ double assemble_tol(const PowSet<K>& s, const AsmCoef& a,
-                                               const double* ch) {
-  if constexpr (K == 0) {
-    return s.A0 * ch[0];
-  } else if constexpr (K == 1) {
-    return fma(s.A1, ch[0], -(a.c11 * s.B1) * ch[1]);
-  } else if constexpr (K == 2) {
-    const double t = fma(-(a.c21 * s.B2), ch[1], s.A2 * ch[0]);
-    return fma(a.c22 * s.C2, ch[2], t);
-  } else {
-    double t = fma(-(a.c31 * s.B3), ch[1], s.A3 * ch[0]);
-    t = fma(a.c32 * s.C3, ch[2], t);
-    return fma(-(a.c33 * s.D3), ch[3], t);
-  }
-}
-
 // parked per-thread fields (see series_kernel)
 constexpr int kRho = 0, kTh = 1, kPwHi = 2, kPwLo = 3, kC1 = 4, kS1 = 5, kCs = 6, kSn = 7;
 constexpr int kPark = 8;
@@ -142,7 +112,9 @@ constexpr int kResident = 3;  // tolerance mode, the WHOLE plan's tables staged
 // kernels fit 64 registers once the group state is parked (4 CTAs, 32 warps)
 template <int K, int NC, int VEC>
 constexpr int series_min_blocks() {
-  return (K == 0 && NC <= 2 && VEC == 2) ? 4 : 3;
+  // several vectors carry 2 x NC running sums per point: 4 and 8 vectors get a
+  // 128-register budget (at 80 they spilled 136 / 788 bytes)
+  return NC >= 4 ? 2 : (K == 0 && NC <= 2 && VEC == 2) ? 4 : 3;
 }
 
 template <int K, bool ANG, int NC, int MODE, int VEC>
@@ -441,7 +413,7 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
     for (int c = 0; c < NC; ++c)
 #pragma unroll
       for (int v = 0; v < VEC; ++v)
-        if (p0 + v < a.P) a.f[p0 + v + (v0 + c) * a.ldf] = acc[c][v];
+        if (p0 + v < a.P && v0 + c < a.ncoef) a.f[p0 + v + (v0 + c) * a.ldf] = acc[c][v];
   }  // tiles
 }
 
@@ -562,19 +534,23 @@ cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nr
     return cudaSuccess;
   }
   for (int v0 = 0; v0 < a.ncoef;) {
+    // the kernel width NC is the smallest of 1, 2, 4, 8 that takes every vector
+    // left (padded with zero coefficients, not stored): 3 vectors as one 4-wide
+    // pass (measured 1.65 ms at config 5) instead of 2 + 1 (2.1 ms)
     const int left = a.ncoef - v0;
-    int nc = left >= 8 ? 8 : left >= 4 ? 4 : left >= 2 ? 2 : 1;
+    int nc = left >= 5 ? 8 : left >= 3 ? 4 : left >= 2 ? 2 : 1;
     // fewer vectors per launch when the stage of nc would not fit; chains too
     // long for any stage read their tables from global memory (buf_doubles 0)
     while (nc > 1 && series_fma_smem_bytes(K, max_jmax, nc, a.exact) > size_t(a.max_smem)) nc >>= 1;
     const bool global = series_fma_smem_bytes(K, max_jmax, nc, a.exact) > size_t(a.max_smem);
     const int buf_doubles = global ? 0 : series_buf_doubles(K, nj, nc, a.exact);
+    const int take = left < nc ? left : nc;  // vectors of this pass (the rest are zero pads)
     if (a.theta)
       series_rowsum_kernel<true><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
-                                                           a.ldc, v0, nc, nc, rowc);
+                                                           a.ldc, v0, take, nc, rowc);
     else
       series_rowsum_kernel<false><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
-                                                            a.ldc, v0, nc, nc, rowc);
+                                                            a.ldc, v0, take, nc, rowc);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     switch (K) {
@@ -585,7 +561,7 @@ cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nr
     }
     if (e != cudaSuccess) return e;
     *launches += 2;
-    v0 += nc;
+    v0 += take;
   }
   return cudaSuccess;
 }

@@ -41,16 +41,22 @@ __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, doubl
 }
 }  // namespace
 
-// NCH chunks of 8 vectors per launch share one recursion (R stays in smem)
-template <int K, bool ANG, int NCH>
+// NCH chunks of 8 vectors per launch share one recursion (R stays in smem).
+// TOL: the series' tolerance-mode recursion (zk_series.cu: plan-resident
+// prescaled coefficients, P_j = fma(fma(a, x, b), P_{j-1}, -c P_{j-2}); for
+// k = 0 the group's rho^|m| scales the DMMA results per point instead of
+// every parked value).
+template <int K, bool ANG, int NCH, bool TOL>
 __global__ void __launch_bounds__(kThreads)
 series_dmma_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int nc,
                    int buf_doubles, int njp_max) {
   constexpr int RS = 2 * kNc * NCH;  // doubles per key record in rowc
+  constexpr int CS = TOL ? 4 : 6;    // doubles per staged chain coefficient
   extern __shared__ __align__(16) double smem[];
   double* s_R = smem + 2 * buf_doubles;        // [key][point], njp_max x kLdp
   double* s_cos = s_R + njp_max * kLdp;        // per point of the tile
   double* s_sin = s_cos + kTile;
+  double* s_a0 = s_sin + kTile;                // rho^|m| per point (TOL, k = 0)
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, t4 = lane & 3;
@@ -73,8 +79,9 @@ series_dmma_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, 
     const GroupRec g = a.groups[gi];
     const int nj = g.jmax + 1;
     double* base = smem + b * buf_doubles;
-    const double* csrc = reinterpret_cast<const double*>(a.coef + g.coef_off);
-    const int ncoef = (K + 1) * nj * 6;
+    const double* csrc = TOL ? reinterpret_cast<const double*>(a.tol + g.coef_off)
+                             : reinterpret_cast<const double*>(a.coef + g.coef_off);
+    const int ncoef = (K + 1) * nj * CS;
     for (int t = tid; t < ncoef; t += kThreads) cp_async8(base + t, csrc + t);
     double* abase = base + ncoef;
     if (K > 0) {
@@ -99,8 +106,17 @@ series_dmma_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, 
     const int nj = jmax + 1;
     const double* base = smem + (gi & 1) * buf_doubles;
     const ChainCoef* s_coef = reinterpret_cast<const ChainCoef*>(base);
-    const AsmCoef* s_asm = reinterpret_cast<const AsmCoef*>(base + (K + 1) * nj * 6);
-    const double* s_rc = base + (K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0);
+    const AsmCoef* s_asm = reinterpret_cast<const AsmCoef*>(base + (K + 1) * nj * CS);
+    const double* s_rc = base + (K + 1) * nj * CS + (K > 0 ? nj * 8 : 0);
+    auto step_at = [&](int i, int d, double p1, double p0) {
+      if constexpr (TOL) {
+        const double2* q = reinterpret_cast<const double2*>(base + (i * nj + d) * 4);
+        const double2 x = q[0], y = q[1];
+        return fma(fma(x.x, u, x.y), p1, -(y.x * p0));
+      } else {
+        return jacobi_step(load_coef(s_coef + i * nj + d), u, p1, p0);
+      }
+    };
 
     const int e_lo = powset_base<K>(alpha);
     if (e_lo > e_cur) pw_acc = dd_mul(pw_acc, dd_pow(rho, e_lo - e_cur));
@@ -112,6 +128,7 @@ series_dmma_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, 
       s_cos[tid] = cs;
       s_sin[tid] = sn;
     }
+    if constexpr (TOL && K == 0) s_a0[tid] = pw.A0;
 
     // radial values R(p, j) of this group into shared memory (sign folded into C)
     auto put = [&](int j, const double(&chs)[K + 1], auto steady) {
@@ -120,7 +137,12 @@ series_dmma_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, 
       double ch[K + 1];
 #pragma unroll
       for (int i = 0; i <= K; ++i) ch[i] = (decltype(steady)::value || j - i >= 0) ? chs[i] : 0.0;
-      s_R[j * kLdp + tid] = assemble<K, K>(pw, ac, ch);
+      if constexpr (TOL && K == 0)
+        s_R[j * kLdp + tid] = ch[0];  // rho^|m| is applied to X, Y per point
+      else if constexpr (TOL)
+        s_R[j * kLdp + tid] = assemble_tol<K>(pw, ac, ch);
+      else
+        s_R[j * kLdp + tid] = assemble<K, K>(pw, ac, ch);
     };
     double A[K + 1], B[K + 1];
 #pragma unroll
@@ -136,7 +158,7 @@ series_dmma_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, 
           A[i] = jacobi_p1(static_cast<double>(alpha + i + 1),
                            static_cast<double>(alpha + 2 * i + 2), u);
         } else if (d >= 2) {
-          const double nx = jacobi_step(load_coef(s_coef + i * nj + d), u, A[i], B[i]);
+          const double nx = step_at(i, d, A[i], B[i]);
           B[i] = A[i];
           A[i] = nx;
         }
@@ -146,18 +168,15 @@ series_dmma_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, 
     int j = K + 2;
     for (; j + 1 <= jmax; j += 2) {
 #pragma unroll
-      for (int i = 0; i <= K; ++i)
-        B[i] = jacobi_step(load_coef(s_coef + i * nj + (j - i)), u, A[i], B[i]);
+      for (int i = 0; i <= K; ++i) B[i] = step_at(i, j - i, A[i], B[i]);
       put(j, B, std::true_type{});
 #pragma unroll
-      for (int i = 0; i <= K; ++i)
-        A[i] = jacobi_step(load_coef(s_coef + i * nj + (j + 1 - i)), u, B[i], A[i]);
+      for (int i = 0; i <= K; ++i) A[i] = step_at(i, j + 1 - i, B[i], A[i]);
       put(j + 1, A, std::true_type{});
     }
     if (j <= jmax) {
 #pragma unroll
-      for (int i = 0; i <= K; ++i)
-        B[i] = jacobi_step(load_coef(s_coef + i * nj + (j - i)), u, A[i], B[i]);
+      for (int i = 0; i <= K; ++i) B[i] = step_at(i, j - i, A[i], B[i]);
       put(j, B, std::true_type{});
     }
     __syncthreads();  // R and the angular factors of the whole tile are in place
@@ -189,6 +208,19 @@ series_dmma_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, 
 #pragma unroll
       for (int mb = 0; mb < 2; ++mb) {
         const int r0 = warp * 32 + mb * 16 + g8;
+        if constexpr (TOL && K == 0) {  // rows r0, r0 + 8: their points' rho^|m|
+          const double f0 = s_a0[r0], f1 = s_a0[r0 + 8];
+          X[mb][0] *= f0;
+          X[mb][1] *= f0;
+          X[mb][2] *= f1;
+          X[mb][3] *= f1;
+          if (ANG) {
+            Y[mb][0] *= f0;
+            Y[mb][1] *= f0;
+            Y[mb][2] *= f1;
+            Y[mb][3] *= f1;
+          }
+        }
         if (ANG) {
           const double c0 = s_cos[r0], s0 = s_sin[r0], c1 = s_cos[r0 + 8], s1 = s_sin[r0 + 8];
           acc[ch][mb][0] = fma(c0, X[mb][0], fma(s0, Y[mb][0], acc[ch][mb][0]));
@@ -218,8 +250,8 @@ series_dmma_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, 
     }
 }
 
-static int dmma_buf_doubles(int K, int nj, int nch) {
-  return ((K + 1) * nj * 6 + (K > 0 ? nj * 8 : 0) + nj * 2 * kNc * nch + 1) & ~1;
+static int dmma_buf_doubles(int K, int nj, int nch, bool exact = true) {
+  return ((K + 1) * nj * (exact ? 6 : 4) + (K > 0 ? nj * 8 : 0) + nj * 2 * kNc * nch + 1) & ~1;
 }
 
 template <int K, bool ANG, int NCH>
@@ -227,9 +259,9 @@ static cudaError_t launch_dmma_one(const SeriesArgs& a, const double* rowc, int 
                                    int max_jmax, cudaStream_t st) {
   const int nj = max_jmax + 1;
   const int njp = (nj + 3) / 4 * 4;
-  const int buf_doubles = dmma_buf_doubles(K, nj, NCH);
-  const size_t smem = (size_t(2) * buf_doubles + size_t(njp) * kLdp + 2 * kTile) * sizeof(double);
-  auto fn = series_dmma_kernel<K, ANG, NCH>;
+  const int buf_doubles = dmma_buf_doubles(K, nj, NCH, a.exact != 0);
+  const size_t smem = (size_t(2) * buf_doubles + size_t(njp) * kLdp + 3 * kTile) * sizeof(double);
+  auto fn = a.exact ? series_dmma_kernel<K, ANG, NCH, false> : series_dmma_kernel<K, ANG, NCH, true>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -243,7 +275,7 @@ int series_dmma_chunks(int ncoef) { return ncoef > 16 ? 4 : ncoef > 8 ? 2 : 1; }
 size_t series_dmma_smem_bytes(int K, int max_jmax, int nch) {
   const int nj = max_jmax + 1;
   const int njp = (nj + 3) / 4 * 4;
-  return (size_t(2) * dmma_buf_doubles(K, nj, nch) + size_t(njp) * kLdp + 2 * kTile) *
+  return (size_t(2) * dmma_buf_doubles(K, nj, nch) + size_t(njp) * kLdp + 3 * kTile) *
          sizeof(double);
 }
 
