@@ -210,3 +210,44 @@ def test_gram_tma_and_cpasync_operand_paths_bitwise(tmp_path):
                         "150000"], check=True, env=env, cwd=root, timeout=600)
         outs.append(np.load(out))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_async_calls_on_different_torch_streams_share_scratch_safely():
+    """Device entry points run on torch's current stream; a context's scratch
+    (Gram panel, series row sums) is shared, so switching streams orders the
+    new stream after the old one's queued work (zk_ctx_set_stream).
+    Back-to-back async Gram/series calls on two streams must equal the
+    synchronous results."""
+    modes = zb.full_mode_set(24)
+    rho, theta = disc(50_000, 9)
+    r_d = torch.from_numpy(rho).cuda()
+    t_d = torch.from_numpy(theta).cuda()
+    c = torch.from_numpy(np.random.default_rng(9).standard_normal(len(modes))).cuda()
+    ref_f = zb.series_device(modes, c, r_d, t_d).clone()
+    ref_G, _ = zb.gram_device(modes, r_d, t_d)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            G1, _ = zb.gram_device(modes, r_d, t_d)
+            f1 = zb.series_device(modes, c, r_d, t_d)
+        with torch.cuda.stream(s2):
+            G2, _ = zb.gram_device(modes, r_d, t_d)
+            f2 = zb.series_device(modes, c, r_d, t_d)
+        outs += [(G1, f1, s1), (G2, f2, s2)]
+    torch.cuda.synchronize()
+    for G, f, _ in outs:
+        assert torch.equal(G, ref_G) and torch.equal(f, ref_f)
+
+
+def test_release_buffers_then_recompute():
+    """release_buffers() frees the host result pool and every context's
+    device scratch / staging ring; the next calls re-allocate transparently."""
+    modes = zb.full_mode_set(30)
+    grid = zb.linear_radial_grid(20_000)
+    a, _ = zb.evaluate_batch(zb.BatchRequest(modes=modes, grid=grid))
+    av = a.values.copy()
+    zb.release_buffers()
+    b, _ = zb.evaluate_batch(zb.BatchRequest(modes=modes, grid=grid))
+    assert np.array_equal(b.values, av)
