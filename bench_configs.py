@@ -12,7 +12,7 @@ roofline, so DESIGN.md / profiles/ can cite every config:
   C5  2-D n=60 x 1e6 disc points: basis (15.1 GB), fused series f = B c,
       Gram B^T B + B^T y (DMMA), Cholesky solve
 
-Peaks: HBM copy 6548.2 GB/s (MEASURED_PEAKS.json), HBM write-only 7321 GB/s
+Peaks: HBM copy from MEASURED_PEAKS.json (6549.8 GB/s this round), HBM write-only 7321 GB/s
 (cudaMemset, tools/hbm_write_probe.cu), FP64 36.9 TFLOP/s (DMMA/DFMA,
 tools/fp64_peak_probe.cu).
 
@@ -32,7 +32,17 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-HBM_COPY = 6548.2
+
+def _copy_peak(default=6549.8):
+    """HBM copy GB/s from the driver-written MEASURED_PEAKS.json (rewritten each round)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return default
+
+
+HBM_COPY = _copy_peak()
 HBM_WRITE = 7321.0
 FP64 = 36.9e12
 

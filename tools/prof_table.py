@@ -15,7 +15,12 @@ import json
 import os
 import sys
 
-HBM_COPY = 6548.2
+try:
+    with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           "MEASURED_PEAKS.json")) as _f:
+        HBM_COPY = float(json.load(_f)["hbm_gbs"])
+except (OSError, KeyError, ValueError):
+    HBM_COPY = 6549.8
 HBM_STORE = 6924.9  # best incompressible streaming-store kernel (profiles/r01_hbm_write_probe.txt)
 
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6,
