@@ -1074,7 +1074,8 @@ int zk_plan_create(zk_ctx* ctx, const int32_t* mode_n, const int32_t* mode_m, in
   size_t off_coef = align_up(off_cols + h.cols.size() * 4, A);
   size_t off_asm = align_up(off_coef + h.coef.size() * sizeof(zk::ChainCoef), A);
   size_t off_tol = align_up(off_asm + h.asmc.size() * sizeof(zk::AsmCoef), A);
-  size_t total = align_up(off_tol + h.tol.size() * sizeof(zk::TolCoef), A) + A;
+  size_t off_tolq = align_up(off_tol + h.tol.size() * sizeof(zk::TolCoef), A);
+  size_t total = align_up(off_tolq + h.tolq.size() * sizeof(zk::TolQ), A) + A;
   std::vector<unsigned char> blob(total, 0);
   auto put = [&](size_t off, const void* src, size_t bytes) {
     if (bytes) std::memcpy(blob.data() + off, src, bytes);
@@ -1086,6 +1087,7 @@ int zk_plan_create(zk_ctx* ctx, const int32_t* mode_n, const int32_t* mode_m, in
   put(off_coef, h.coef.data(), h.coef.size() * sizeof(zk::ChainCoef));
   put(off_asm, h.asmc.data(), h.asmc.size() * sizeof(zk::AsmCoef));
   put(off_tol, h.tol.data(), h.tol.size() * sizeof(zk::TolCoef));
+  put(off_tolq, h.tolq.data(), h.tolq.size() * sizeof(zk::TolQ));
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e == cudaSuccess) e = cudaMalloc(&plan->dmem, total);
   if (e == cudaSuccess) e = cudaMemcpy(plan->dmem, blob.data(), total, cudaMemcpyHostToDevice);
@@ -1102,6 +1104,7 @@ int zk_plan_create(zk_ctx* ctx, const int32_t* mode_n, const int32_t* mode_m, in
   plan->coef = reinterpret_cast<const zk::ChainCoef*>(base + off_coef);
   plan->asmc = reinterpret_cast<const zk::AsmCoef*>(base + off_asm);
   plan->tol = reinterpret_cast<const zk::TolCoef*>(base + off_tol);
+  plan->tolq = reinterpret_cast<const zk::TolQ*>(base + off_tolq);
   *out = plan;
   return ZK_OK;
 }
@@ -1202,6 +1205,7 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const do
     a.coef = plan->coef;
     a.asmc = plan->asmc;
     a.tol = plan->tol;
+    a.tolq = env_int("ZK_SERIES_SCALED", 1) ? plan->tolq : nullptr;
     a.rho = d_rho;
     a.theta = d_theta;
     a.c = d_coef;
@@ -1215,6 +1219,7 @@ int zk_series_eval(zk_ctx* ctx, const zk_plan* plan, const double* rho, const do
     a.sms = ctx->sm_count;
     a.resident = env_int("ZK_SERIES_RESIDENT", 0);
     a.vec3 = env_int("ZK_SERIES_VEC3", 1);
+    a.k0 = env_int("ZK_SERIES_K0", 3);
     a.ntol = static_cast<int>(plan->host.tol.size());
     a.nasm = static_cast<int>(plan->host.asmc.size());
     a.nrows = static_cast<int>(plan->host.rowptr.size());

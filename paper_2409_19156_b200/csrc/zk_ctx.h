@@ -74,6 +74,7 @@ struct zk_plan {
   const zk::ChainCoef* coef = nullptr;
   const zk::AsmCoef* asmc = nullptr;
   const zk::TolCoef* tol = nullptr;
+  const zk::TolQ* tolq = nullptr;
   // Unique-column views for host outputs of the radial basis (built on first
   // use): the kernel writes the "sent" columns -- one per unique (n, |m|)
   // key, its first column, plus optionally a share of the repeated columns --

@@ -27,10 +27,22 @@ static_assert(sizeof(ChainCoef) == 48, "ChainCoef layout");
 // Tolerance-mode form of the same step (series kernel, zk_series.cu):
 // P_j = (a x + b) P_{j-1} - c P_{j-2} with a = mid_x/lead, b = mid_const/lead,
 // c = last/lead, each the correctly rounded quotient of exact integers.
+// s: the chain's scale s_j = c_j s_{j-2} (s_0 = s_1 = 1) of the scaled form
+// below; the series multiplies the chain-0 row coefficients by it.
 struct alignas(16) TolCoef {
-  double a, b, c, pad;
+  double a, b, c, s;
 };
 static_assert(sizeof(TolCoef) == 32, "TolCoef layout");
+
+// Scaled tolerance-mode chain (the k = 0 series): Q_j = P_j / s_j obeys
+// Q_j = (a' x + b') Q_{j-1} - Q_{j-2} with a' = a s_{j-1}/s_j, b' = b s_{j-1}/s_j
+// -- 2 FP64 instructions per step (no c P_{j-2} product). s_j stays in
+// [0.01, 1] for every chain up to degree 6000 (alpha <= 5000). Degree 1 holds
+// P_1's own (a', b') so a chain can start from Q_0 = 1, Q_-1 = 0.
+struct alignas(16) TolQ {
+  double a, b;
+};
+static_assert(sizeof(TolQ) == 16, "TolQ layout");
 
 // Derivative prefactors per jacobi degree j of a group (zk/evaluate.py:127-149);
 // every product is an exact integer or half-integer in binary64.
@@ -76,6 +88,7 @@ struct HostPlan {
   std::vector<int32_t> cols;          // column*2 + (m < 0)
   std::vector<ChainCoef> coef;        // per group: (max_order+1) x (jmax+1)
   std::vector<TolCoef> tol;           // same indexing as coef
+  std::vector<TolQ> tolq;             // same indexing as coef
   std::vector<AsmCoef> asmc;          // per group: (jmax+1)
 };
 

@@ -49,6 +49,7 @@ struct SeriesArgs {
   const ChainCoef* coef;
   const AsmCoef* asmc;
   const TolCoef* tol;     // tolerance-mode coefficients (same indexing as coef)
+  const TolQ* tolq;       // scaled chains (k = 0 tolerance mode); nullptr: unscaled
   const double* rho;
   const double* theta;    // nullptr: radial basis
   const double* c;        // M x ncoef, column-major, ldc
@@ -62,6 +63,7 @@ struct SeriesArgs {
   int sms;                // SM count
   int resident;           // allow the whole-plan resident stage (tolerance mode)
   int vec3;               // 3 points per thread for the k = 0 single-vector kernel
+  int k0;                 // k = 0 single-vector resident kernel: points per thread (2, 3), 0 off
   int ntol, nasm, nrows;  // plan table sizes: TolCoef/ChainCoef, AsmCoef, row slots
 };
 
@@ -70,6 +72,11 @@ size_t series_scratch_bytes(long long nrowslots);
 size_t series_fma_smem_bytes(int K, int max_jmax, int nc, bool exact);
 cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nrowslots,
                           double* rowc, bool dmma, cudaStream_t st, int* launches);
+// k = 0, one coefficient vector, whole plan resident in shared memory
+// (zk_series_k0.cu); cudaErrorNotSupported when the request does not qualify
+size_t series_k0_smem_bytes(long long nrows, int ngroups, int vec);
+cudaError_t launch_series_k0(const SeriesArgs& a, long long nrows, double* scratch, int vec,
+                             cudaStream_t st, int* launches);
 int series_dmma_chunks(int ncoef);
 size_t series_dmma_smem_bytes(int K, int max_jmax, int nch);
 cudaError_t launch_series_dmma(const SeriesArgs& a, int K, int nch, int v0, int nc, int max_jmax,

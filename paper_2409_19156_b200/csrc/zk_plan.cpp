@@ -224,6 +224,30 @@ std::string build_plan(const int32_t* n, const int32_t* m, int64_t M, int max_or
         P.coef.push_back(cc);
         P.tol.push_back(tc);
       }
+      // scaled form of this chain (TolQ): s_j = c_j s_{j-2}, rounded once;
+      // a', b' from the stored scales so P_j = s_j Q_j up to one rounding
+      // per coefficient
+      const size_t c0 = P.tol.size() - static_cast<size_t>(g.jmax + 1);
+      for (int64_t j = 0; j <= g.jmax; ++j) {
+        TolCoef& tc = P.tol[c0 + static_cast<size_t>(j)];
+        TolQ q{};
+        if (j < 2) {
+          tc.s = 1.0;
+          if (j == 1) {  // P_1 = (a+b+2)/2 x + (a-b)/2: the uniform step from Q_0 = 1, Q_-1 = 0
+            q.a = 0.5 * static_cast<double>(a + b + 2);
+            q.b = 0.5 * static_cast<double>(a - b);
+          }
+        } else {
+          const ChainCoef& cc = P.coef[c0 + static_cast<size_t>(j)];
+          const long double sm2 = P.tol[c0 + static_cast<size_t>(j - 2)].s;
+          const long double sm1 = P.tol[c0 + static_cast<size_t>(j - 1)].s;
+          tc.s = static_cast<double>(static_cast<long double>(cc.last) / cc.lead * sm2);
+          const long double r = sm1 / static_cast<long double>(tc.s);
+          q.a = static_cast<double>(static_cast<long double>(cc.mid_x) / cc.lead * r);
+          q.b = static_cast<double>(static_cast<long double>(cc.mid_const) / cc.lead * r);
+        }
+        P.tolq.push_back(q);
+      }
     }
     g.asm_off = static_cast<int32_t>(P.asmc.size());
     const double md = static_cast<double>(g.alpha);

@@ -75,11 +75,13 @@ __global__ void series_rowsum_kernel(const GroupRec* __restrict__ groups,
                                      const int32_t* __restrict__ rowptr,
                                      const int32_t* __restrict__ cols,
                                      const double* __restrict__ c, long long ldc, int v0, int nc,
-                                     int stride, double* __restrict__ rowc) {
+                                     int stride, const TolCoef* __restrict__ scale,
+                                     double* __restrict__ rowc) {
   const GroupRec g = groups[blockIdx.x];
   for (int j = threadIdx.x; j <= g.jmax; j += blockDim.x) {
     const int r_lo = rowptr[g.row0 + j], r_hi = rowptr[g.row0 + j + 1];
-    const double sgn = (j & 1) ? -1.0 : 1.0;
+    // scaled chains (kTolQ): the kernel folds Q_j = P_j / s_j, so C carries s_j
+    const double sgn = ((j & 1) ? -1.0 : 1.0) * (scale ? scale[g.coef_off + j].s : 1.0);
     for (int v = 0; v < stride; ++v) {
       double cp = 0.0, cn = 0.0;
       if (v < nc) {
@@ -107,6 +109,8 @@ constexpr int kGlobal = 2;  // K1-identical, tables read from global memory
 constexpr int kResident = 3;  // tolerance mode, the WHOLE plan's tables staged
                               // once per CTA: no per-group barrier; persistent
                               // CTAs walk several point tiles
+constexpr int kTolQ = 4;      // k = 0 tolerance mode on the scaled chains (TolQ):
+                              // 2 FP64 instructions per step, 16-byte coefficients
 
 // CTAs per SM the register budget is sized for: the k = 0, few-vector
 // kernels fit 64 registers once the group state is parked (4 CTAs, 32 warps)
@@ -121,10 +125,12 @@ template <int K, bool ANG, int NC, int MODE, int VEC>
 __global__ void __launch_bounds__(kThreads, series_min_blocks<K, NC, VEC>())
 series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int buf_doubles) {
   constexpr bool RES = MODE == kResident;
-  constexpr bool TOL = MODE == kTol || RES;
+  constexpr bool SCALED = MODE == kTolQ;
+  static_assert(!SCALED || K == 0, "scaled chains: k = 0 only");
+  constexpr bool TOL = MODE == kTol || RES || SCALED;
   constexpr bool GLB = MODE == kGlobal;
   constexpr bool STAGED = !GLB && !RES;  // per-group double-buffered stage
-  constexpr int CS = TOL ? 4 : 6;  // doubles per staged chain coefficient
+  constexpr int CS = SCALED ? 2 : TOL ? 4 : 6;  // doubles per staged chain coefficient
   extern __shared__ __align__(16) double smem_all[];
   // per-thread group-level state parked in shared memory while the steady
   // loop runs (frees ~30 registers for the chains, the sums and the
@@ -197,7 +203,10 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
       const int nj = g.jmax + 1;
       double* base = smem + b * buf_doubles;
       const int ncoef = (K + 1) * nj * CS;
-      if constexpr (TOL) {  // the plan's prescaled coefficients (TolCoef)
+      if constexpr (SCALED) {  // the scaled chains' (a', b')
+        const double* tsrc = reinterpret_cast<const double*>(a.tolq + g.coef_off);
+        for (int t = tid; t < ncoef; t += kThreads) cp_async8(base + t, tsrc + t);
+      } else if constexpr (TOL) {  // the plan's prescaled coefficients (TolCoef)
         const double* tsrc = reinterpret_cast<const double*>(a.tol + g.coef_off);
         for (int t = tid; t < ncoef; t += kThreads) cp_async8(base + t, tsrc + t);
       } else {
@@ -241,7 +250,10 @@ series_kernel(const SeriesArgs a, const double* __restrict__ rowc, int v0, int b
                                  : base + (K + 1) * nj * CS + (K > 0 ? nj * 8 : 0);
       // chain step of chain i to degree d (exact or tolerance mode)
       auto step_at = [&](int i, int d, double x, double p1, double p0) {
-        if constexpr (TOL) {
+        if constexpr (SCALED) {
+          const double2 q = *reinterpret_cast<const double2*>(base + (i * nj + d) * 2);
+          return fma(fma(q.x, x, q.y), p1, -p0);
+        } else if constexpr (TOL) {
           return jacobi_step_tol(load_tol(base + (i * nj + d) * 4), x, p1, p0);
         } else {
           return jacobi_step(load_coef(s_coef + i * nj + d), x, p1, p0);
@@ -422,6 +434,12 @@ static long long resident_doubles(const SeriesArgs& a, int K, int nc) {
   return 4LL * (K + 1) * a.nasm + (K > 0 ? 8LL * a.nasm : 0) + 2LL * nc * a.nrows;
 }
 
+// the k = 0 tolerance-mode series runs on the scaled chains (kTolQ) whenever
+// its tables are staged; the row coefficients then carry s_j (rowsum)
+static bool series_scaled(const SeriesArgs& a, int K, int buf_doubles) {
+  return K == 0 && !a.exact && a.tolq != nullptr && buf_doubles > 0;
+}
+
 template <int K, bool ANG, int NC, int VEC>
 static cudaError_t launch_vec(const SeriesArgs& a, const double* rowc, int v0, int buf_doubles,
                               cudaStream_t st) {
@@ -431,10 +449,12 @@ static cudaError_t launch_vec(const SeriesArgs& a, const double* rowc, int v0, i
   const size_t park = size_t(kPark) * VEC * kThreads * sizeof(double);
   size_t smem = park + size_t(2) * buf_doubles * sizeof(double);
   auto fn = a.exact ? series_kernel<K, ANG, NC, kExact, VEC> : series_kernel<K, ANG, NC, kTol, VEC>;
+  if constexpr (K == 0)
+    if (series_scaled(a, K, buf_doubles)) fn = series_kernel<K, ANG, NC, kTolQ, VEC>;
   if (buf_doubles == 0) {  // long chains: global-table variant, one vector per launch
     if constexpr (NC != 1 || VEC != 2) return cudaErrorInvalidValue;
     fn = series_kernel<K, ANG, 1, kGlobal, 2>;
-  } else if (!a.exact && a.resident) {
+  } else if (!a.exact && a.resident && !series_scaled(a, K, buf_doubles)) {
     // the whole plan fits: stage it once per CTA, persistent CTAs over the tiles
     const size_t rs = park + size_t(resident_doubles(a, K, NC)) * sizeof(double);
     if (rs <= size_t(a.max_smem)) {
@@ -494,8 +514,8 @@ static cudaError_t launch_ang(const SeriesArgs& a, const double* rowc, int v0, i
                  : launch_nc<K, false>(a, rowc, v0, nc, buf_doubles, st);
 }
 
-// doubles of one group's stage: (K+1) x nj chain coefficients, nj AsmCoef,
-// nj x 2nc row coefficients
+// doubles of one group's stage: (K+1) x nj chain coefficients (6 exact, 4
+// tolerance, 2 scaled), nj AsmCoef, nj x 2nc row coefficients
 static int series_buf_doubles(int K, int nj, int nc, bool exact) {
   return ((K + 1) * nj * (exact ? 6 : 4) + (K > 0 ? nj * 8 : 0) + nj * 2 * nc + 1) & ~1;
 }
@@ -512,9 +532,12 @@ size_t series_scratch_bytes(long long nrowslots) {
 
 cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nrowslots,
                           double* rowc, bool dmma, cudaStream_t st, int* launches) {
-  (void)nrowslots;
   if (a.P <= 0) return cudaSuccess;
   const int nj = max_jmax + 1;
+  if (!dmma && K == 0 && a.k0 > 0) {
+    const cudaError_t e = launch_series_k0(a, nrowslots, rowc, a.k0, st, launches);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (dmma) {  // tensor-core path: up to 32 vectors per launch, zero-padded to 8s
     const int nch = series_dmma_chunks(a.ncoef);
     const int per = 8 * nch;
@@ -522,10 +545,10 @@ cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nr
       const int nc = a.ncoef - v0 < per ? a.ncoef - v0 : per;
       if (a.theta)
         series_rowsum_kernel<true><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
-                                                             a.ldc, v0, nc, per, rowc);
+                                                             a.ldc, v0, nc, per, nullptr, rowc);
       else
         series_rowsum_kernel<false><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
-                                                              a.ldc, v0, nc, per, rowc);
+                                                              a.ldc, v0, nc, per, nullptr, rowc);
       cudaError_t e = cudaGetLastError();
       if (e == cudaSuccess) e = launch_series_dmma(a, K, nch, v0, nc, max_jmax, rowc, st);
       if (e != cudaSuccess) return e;
@@ -545,12 +568,13 @@ cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nr
     const bool global = series_fma_smem_bytes(K, max_jmax, nc, a.exact) > size_t(a.max_smem);
     const int buf_doubles = global ? 0 : series_buf_doubles(K, nj, nc, a.exact);
     const int take = left < nc ? left : nc;  // vectors of this pass (the rest are zero pads)
+    const TolCoef* scale = series_scaled(a, K, buf_doubles) ? a.tol : nullptr;
     if (a.theta)
       series_rowsum_kernel<true><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
-                                                           a.ldc, v0, take, nc, rowc);
+                                                           a.ldc, v0, take, nc, scale, rowc);
     else
       series_rowsum_kernel<false><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.c,
-                                                            a.ldc, v0, take, nc, rowc);
+                                                            a.ldc, v0, take, nc, scale, rowc);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     switch (K) {

@@ -1,0 +1,288 @@
+// K3, single coefficient vector, k = 0: f = B c for the 2-D (or radial) basis
+// with the whole plan resident in shared memory (config 5).
+//
+// The general series kernel (zk_series.cu) stages each alpha group's tables
+// with a CTA barrier and parks the per-point group state in shared memory; at
+// config 5 (61 groups of ~16 keys) that per-group work was more instructions
+// than the keys themselves. This kernel removes it:
+//
+//  * one table of 32-byte key records {a', b', s C+, s C-} (row slot order,
+//    series_rec_kernel) plus the group records are loaded into shared memory
+//    ONCE per CTA by a bulk copy (cp.async.bulk, SASS UBLKCP) on an mbarrier;
+//    no per-group staging or barrier;
+//  * the chains run on the scaled form (TolQ, zk_internal.h):
+//    Q_j = fma(fma(a', x, b'), Q_{j-1}, -Q_{j-2}) from Q_0 = 1, Q_-1 = 0 --
+//    P_j = s_j Q_j, and s_j is folded into the record's coefficients -- so a
+//    (key, point) costs 4 FP64 instructions: the step's two FMAs and the two
+//    group sums X += Q C+, Y += Q C-;
+//  * the group's rho^|m| cos(|m| theta), rho^|m| sin(|m| theta) is ONE complex
+//    number w = z^alpha, z = rho e^{i theta}, advanced by a complex multiply
+//    per alpha step and re-anchored on the exact rho^alpha (double-double,
+//    ascending) times sincos(fl(alpha theta)) at least every 8 alpha-steps --
+//    the same anchoring policy as the general kernel's rotation; per group
+//    f += X Re(w) + Y Im(w).
+// Tolerance semantics as the general kernel's tolerance mode: same sums,
+// different rounding (tests/test_gpu_series.py measures it against binary128).
+#include <cuda_runtime.h>
+
+#include "zk_kernels.cuh"
+#include "zk_launch.h"
+
+namespace zk {
+
+namespace {
+constexpr int kT = 256;
+constexpr int kPark0 = 4;  // parked per point: rho, theta, (rho^e hi, lo) of the last anchor
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+}  // namespace
+
+// rec[row0 + j] = {a'_j, b'_j, (-1)^j s_j C+_j, (-1)^j s_j C-_j} of chain 0 for
+// every key (alpha, j) of the plan (one CTA per group, a thread per degree)
+template <bool ANG>
+__global__ void series_rec_kernel(const GroupRec* __restrict__ groups,
+                                  const int32_t* __restrict__ rowptr,
+                                  const int32_t* __restrict__ cols, const TolQ* __restrict__ tolq,
+                                  const TolCoef* __restrict__ tol, const double* __restrict__ c,
+                                  double4* __restrict__ rec) {
+  const GroupRec g = groups[blockIdx.x];
+  for (int j = threadIdx.x; j <= g.jmax; j += blockDim.x) {
+    double cp = 0.0, cn = 0.0;
+    for (int r = rowptr[g.row0 + j]; r < rowptr[g.row0 + j + 1]; ++r) {
+      const int code = cols[r];
+      const double x = c[code >> 1];
+      if (ANG && (code & 1)) cn += x; else cp += x;
+    }
+    const double s = ((j & 1) ? -1.0 : 1.0) * tol[g.coef_off + j].s;
+    const TolQ q = tolq[g.coef_off + j];
+    rec[g.row0 + j] = make_double4(q.a, q.b, s * cp, s * cn);
+  }
+}
+
+// One pass over the whole plan for V points per thread: points p0 .. p0+V-1
+// (those below pend). Per-point state in registers; the anchor state is
+// parked in shared memory (park[(f V + v) kT + tid]).
+template <bool ANG, int V>
+__device__ __forceinline__ void k0_points(const SeriesArgs& a, const GroupRec* grp,
+                                          const double4* tab, double* park, long long p0,
+                                          long long pend, const unsigned long long* bar) {
+  const int tid = threadIdx.x;
+  auto pk = [&](int f, int v) -> double& { return park[(f * V + v) * kT + tid]; };
+  double u[V], zr[V], zi[V], wr[V], wi[V], acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const bool live = p0 + v < pend;
+    const double r = live ? __ldg(a.rho + p0 + v) : 0.0;
+    const double t = (ANG && live) ? __ldg(a.theta + p0 + v) : 0.0;
+    u[v] = jacobi_u(r);
+    if constexpr (ANG) {
+      double s1, c1;
+      sincos(t, &s1, &c1);
+      zr[v] = r * c1;
+      zi[v] = r * s1;
+    } else {
+      zr[v] = r;
+      zi[v] = 0.0;
+    }
+    wr[v] = 1.0;
+    wi[v] = 0.0;
+    acc[v] = 0.0;
+    pk(0, v) = r;
+    pk(1, v) = t;
+    pk(2, v) = 1.0;
+    pk(3, v) = 0.0;
+  }
+  if (bar)  // first pass: the tables' bulk copy lands while the points load
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        "@!p bra W_%=;\n}\n" ::"r"(smem_u32(bar))
+        : "memory");
+  int a_cur = -1, e_cur = 0, since = 0;
+  for (int gi = 0; gi < a.ngroups; ++gi) {
+    const GroupRec g = grp[gi];
+    const int alpha = g.alpha;
+    const int step = alpha - a_cur;  // CTA-uniform
+    if (step != 0) {
+      if (a_cur >= 0 && step > 0 && step <= 4 && since + step <= 8) {
+#pragma unroll 1
+        for (int s = 0; s < step; ++s) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if constexpr (ANG) {
+              const double nr = fma(wr[v], zr[v], -(wi[v] * zi[v]));
+              wi[v] = fma(wr[v], zi[v], wi[v] * zr[v]);
+              wr[v] = nr;
+            } else {
+              wr[v] *= zr[v];
+            }
+          }
+        }
+        since += step;
+      } else {
+        // anchor: rho^alpha in double-double (ascending exponents), exact angle
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const double r = pk(0, v);
+          dd p{pk(2, v), pk(3, v)};
+          if (alpha >= e_cur) {
+            if (alpha == e_cur + 1) p = dd_mul_d(p, r);
+            else if (alpha > e_cur) p = dd_mul(p, dd_pow(r, alpha - e_cur));
+          } else {
+            p = dd_pow(r, alpha);
+          }
+          pk(2, v) = p.hi;
+          pk(3, v) = p.lo;
+          if constexpr (ANG) {
+            double sn, cs;
+            sincos(__dmul_rn(static_cast<double>(alpha), pk(1, v)), &sn, &cs);
+            wr[v] = p.hi * cs;
+            wi[v] = p.hi * sn;
+          } else {
+            wr[v] = p.hi;
+          }
+        }
+        e_cur = alpha;
+        since = 0;
+      }
+      a_cur = alpha;
+    }
+
+    // the group's keys: X = sum Q C+, Y = sum Q C-; degrees 0 and 1 peeled
+    // (Q_0 = 1, Q_1 = a'_1 x + b'_1)
+    const double4* R = tab + g.row0;
+    const int jmax = g.jmax;
+    double gx[V], gy[V], q1[V], q0[V];
+    {
+      const double2 c0 = *reinterpret_cast<const double2*>(&R[0].z);
+      if (jmax >= 1) {
+        const double2 ab = *reinterpret_cast<const double2*>(&R[1].x);
+        const double2 cc = *reinterpret_cast<const double2*>(&R[1].z);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          q0[v] = 1.0;
+          q1[v] = fma(ab.x, u[v], ab.y);
+          gx[v] = fma(q1[v], cc.x, c0.x);
+          gy[v] = fma(q1[v], cc.y, c0.y);
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          gx[v] = c0.x;
+          gy[v] = c0.y;
+          q1[v] = q0[v] = 0.0;
+        }
+      }
+    }
+#pragma unroll 4
+    for (int j = 2; j <= jmax; ++j) {
+      const double2 ab = *reinterpret_cast<const double2*>(&R[j].x);
+      const double2 cc = *reinterpret_cast<const double2*>(&R[j].z);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const double qn = fma(fma(ab.x, u[v], ab.y), q1[v], -q0[v]);
+        q0[v] = q1[v];
+        q1[v] = qn;
+        gx[v] = fma(qn, cc.x, gx[v]);
+        if (ANG) gy[v] = fma(qn, cc.y, gy[v]);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      acc[v] = fma(gx[v], wr[v], acc[v]);
+      if (ANG) acc[v] = fma(gy[v], wi[v], acc[v]);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+    if (p0 + v < pend) a.f[p0 + v] = acc[v];
+}
+
+// One CTA per tile of kT x VEC points (VEC 3: 2.9 waves of 444 CTA slots at
+// config 5). Measured and not kept: persistent CTAs over equal contiguous
+// shares walked in passes of 4 points per thread plus a 2-point remainder
+// pass (0.447 vs 0.413 ms), and 4 points per thread in 3.3 waves (0.416).
+template <bool ANG, int VEC>
+__global__ void __launch_bounds__(kT, VEC >= 4 ? 2 : 3)
+series_k0_kernel(const SeriesArgs a, const double4* __restrict__ rec, int nrows) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) unsigned long long bar;
+  const int tid = threadIdx.x;
+  double* park = sm;
+  const double4* tab = reinterpret_cast<const double4*>(sm + kPark0 * VEC * kT);
+  const GroupRec* grp = reinterpret_cast<const GroupRec*>(tab + nrows);
+
+  // the key records and group records: one bulk copy each, one mbarrier
+  const unsigned tab_bytes = static_cast<unsigned>(nrows) * 32u;
+  const unsigned grp_bytes = static_cast<unsigned>(a.ngroups) * 32u;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
+                 "r"(tab_bytes + grp_bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(tab)),
+        "l"(rec), "r"(tab_bytes), "r"(smem_u32(&bar))
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(grp)),
+        "l"(a.groups), "r"(grp_bytes), "r"(smem_u32(&bar))
+        : "memory");
+  }
+  const long long ntiles = (a.P + kT * VEC - 1) / (kT * VEC);
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+    k0_points<ANG, VEC>(a, grp, tab, park, tile * (kT * VEC) + tid * VEC, a.P,
+                        tile == blockIdx.x ? &bar : nullptr);
+}
+
+size_t series_k0_smem_bytes(long long nrows, int ngroups, int vec) {
+  return size_t(kPark0) * vec * kT * sizeof(double) + size_t(nrows) * 32 + size_t(ngroups) * 32;
+}
+
+template <bool ANG, int VEC>
+static cudaError_t launch_k0(const SeriesArgs& a, const double4* rec, int nrows, size_t smem,
+                             cudaStream_t st) {
+  auto fn = series_k0_kernel<ANG, VEC>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const long long ntiles = (a.P + kT * VEC - 1) / (kT * VEC);
+  fn<<<static_cast<unsigned>(ntiles), kT, smem, st>>>(a, rec, nrows);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_series_k0(const SeriesArgs& a, long long nrows, double* scratch, int vec,
+                             cudaStream_t st, int* launches) {
+  const size_t smem = series_k0_smem_bytes(nrows, a.ngroups, vec);
+  if (a.ncoef != 1 || a.exact || !a.tolq || smem > size_t(a.max_smem))
+    return cudaErrorNotSupported;
+  if (a.P <= 0) return cudaSuccess;
+  double4* rec = reinterpret_cast<double4*>(scratch);
+  if (a.theta)
+    series_rec_kernel<true><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.tolq, a.tol,
+                                                       a.c, rec);
+  else
+    series_rec_kernel<false><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.tolq, a.tol,
+                                                        a.c, rec);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int n = static_cast<int>(nrows);
+  if (a.theta)
+    e = vec == 2   ? launch_k0<true, 2>(a, rec, n, smem, st)
+        : vec == 4 ? launch_k0<true, 4>(a, rec, n, smem, st)
+                   : launch_k0<true, 3>(a, rec, n, smem, st);
+  else
+    e = vec == 2   ? launch_k0<false, 2>(a, rec, n, smem, st)
+        : vec == 4 ? launch_k0<false, 4>(a, rec, n, smem, st)
+                   : launch_k0<false, 3>(a, rec, n, smem, st);
+  if (e == cudaSuccess) *launches += 2;
+  return e;
+}
+
+}  // namespace zk

@@ -25,7 +25,7 @@ run k1_c3_k3   radial_basis  2 python tools/run_config.py 100 100000 3 0 3
 run k1_c3_all  radial_basis  2 python tools/run_config.py 100 100000 3 1 3
 run k1_c4      radial_basis  2 python tools/run_config.py 200 10000 0 0 3
 run k2_c5      radial_basis  2 python tools/run_config.py 60 1000000 0 0 3 1
-run k3_series  series_kernel 2 python tools/run_series.py
+run k3_series  "series_(k0_)?kernel" 2 python tools/run_series.py
 run k4_syrk    "syrk_(tma|partial)"  0 python tools/run_gram.py
 run k4_reduce  syrk_reduce   0 python tools/run_gram.py
 run k3_series_dmma series_dmma  2 python tools/run_misc.py dmma
