@@ -134,6 +134,60 @@ def test_series_fma_and_dmma_paths(monkeypatch, path, k, V):
         assert (np.abs(f - ref) <= 1e-13 * scale + 1e-13).all(), (path, k, V, th is None)
 
 
+ENGINES = {  # single-vector k = 0 series engines (environment switches read per call)
+    "resident3": {},
+    "resident2": {"ZK_SERIES_K0": "2"},
+    "resident4": {"ZK_SERIES_K0": "4"},
+    "staged_scaled": {"ZK_SERIES_K0": "0"},
+    "staged_unscaled": {"ZK_SERIES_K0": "0", "ZK_SERIES_SCALED": "0"},
+    "exact": {"ZK_SERIES_EXACT": "1"},
+}
+
+
+@pytest.mark.parametrize("engine", sorted(ENGINES))
+def test_series_k0_engines_edge_cases(monkeypatch, engine):
+    """Every single-vector k = 0 engine against B @ c of the oracle: the
+    resident kernel (zk_series_k0.cu) at 2/3/4 points per thread, the staged
+    kernel on scaled and unscaled chains, and the exact arithmetic. Sparse
+    alpha sets (rotation steps > 1 and anchors after jumps > 4), a group split
+    into virtual groups (> 4096 duplicated columns), rho = 0 and 1, point
+    counts that are not tile multiples, 2-D and radial."""
+    for k, v in ENGINES[engine].items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(5)
+    sparse = [(n, m) for n, m in [(0, 0), (1, 1), (7, -1), (9, 3), (12, -2), (30, 8), (31, -9),
+                                  (31, 13), (40, 22), (44, -24), (45, 25), (60, 60), (61, -59)]]
+    dup = [(6, 2)] * 4200 + [(6, -2)] * 300 + [(5, 1), (9, -3)]
+    for pairs in (sparse, dup):
+        modes = zb.as_mode_set(pairs)
+        c = rng.standard_normal(len(modes))
+        for P in (1, 255, 769, 2049):
+            rho, theta = disc(P, P)
+            rho[0] = 0.0
+            if P > 1:
+                rho[1] = 1.0
+            for th in (theta, None):
+                f = zb.series_eval(modes, c, rho, th)
+                B = orc.basis_2d(pairs, rho, theta) if th is not None else orc.radial_batch(pairs, rho, 0)
+                scale = np.abs(B) @ np.abs(c)
+                assert (np.abs(f - B @ c) <= 1e-13 * scale + 1e-300).all(), (engine, len(pairs), P, th is None)
+    modes = zb.full_mode_set(8)
+    assert zb.series_eval(modes, np.ones(len(modes)), np.zeros(0), np.zeros(0)).shape == (0,)
+
+
+def test_series_resident_table_too_large_falls_back(monkeypatch):
+    """n = 200 (20,301 modes): the key-record table (10,402 rows x 32 B) does not
+    fit one CTA's shared memory; the staged kernel takes the request."""
+    modes = zb.full_mode_set(200)
+    pairs = [(md.n, md.m) for md in modes]
+    rho, theta = disc(300, 9)
+    c = np.random.default_rng(9).standard_normal(len(modes))
+    f = zb.series_eval(modes, c, rho, theta)
+    B = orc.basis_2d(pairs, rho, theta)
+    scale = np.abs(B) @ np.abs(c)
+    assert (np.abs(f - B @ c) <= 1e-12 * scale).all()
+
+
 @pytest.mark.parametrize("V", [1, 3])
 def test_series_long_chains_any_degree(V):
     """Chains whose tables exceed the shared-memory stage (n = 3000, k = 3)
