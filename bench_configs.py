@@ -175,7 +175,11 @@ def main():
         results.append({"config": "C5 series f=Bc (fused)", "P": P, "M": M, "ms": t * 1e3,
                         "evals_per_s": P * M / t, "alg_fp64_tflops": fl / t / 1e12,
                         "frac_fp64": fl / t / FP64, "bound": "fp64",
-                        "note": "B never materialised; materialise+GEMV would move 2x15.1 GB"})
+                        "note": "B never materialised; materialise+GEMV would move 2x15.1 GB. "
+                                "alg_fp64 is the SURVEY 8d count (6 FP64 ops per exact "
+                                "recursion step); the scaled recursion executes 2 per step, so "
+                                "it can exceed the FP64 peak -- the FP64 pipe utilisation is "
+                                "in the ncu capture (profiles/r02/kernels.md)"})
         y = torch.empty(P, dtype=torch.float64, device="cuda")
         series()
         torch.cuda.synchronize()
