@@ -370,7 +370,7 @@ def run_c5fit(args, world, rank, local, dist, stream, comm):
     if dist:
         phase = np.array([max_over_ranks(dist, float(v), local) for v in phase])
     err = float((x.cpu() - torch.from_numpy(coef_h)).abs().max())
-    nb = (M + 1 + 127) // 128
+    nb = (M + 1 + 63) // 64  # 64 x 64 upper-triangle blocks of [B y] (zk_gram.cu BM)
     alg = 1.0 * P_C5 / world * (M + 1) * (M + 2)  # triangle of [B y]^T [B y], this rank
     return {"workload": f"config 5: 2-D basis n<={N_C5} ({M} modes) on {P_C5} disc points "
                         f"(rho=sqrt(U), theta=2 pi V, seed 0), {hi - lo} per GPU; y = B c, "
