@@ -195,8 +195,9 @@ def main():
                                                    r.data_ptr(), _lib.ZK_ASYNC), "gram")
 
         t = timed(gram, 3, warm=1)
-        nb = (M + 1 + 127) // 128
-        exe = 2.0 * P * (nb * (nb + 1) // 2) * 128 * 128
+        bm = 64  # G block edge of the SYRK tiles (zk_gram.cu BM; 128 in round 1)
+        nb = (M + 1 + bm - 1) // bm
+        exe = 2.0 * P * (nb * (nb + 1) // 2) * bm * bm
         alg = 1.0 * P * (M + 1) * (M + 2)  # triangle of [B y]^T [B y]
         results.append({"config": "C5 Gram B^T B + B^T y (DMMA)", "P": P, "M": M, "ms": t * 1e3,
                         "alg_fp64_tflops_triangle": alg / t / 1e12,
