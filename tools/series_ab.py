@@ -1,5 +1,6 @@
 """A/B timing of the config-5 series (one coefficient vector, device-resident,
 CUDA events) under environment switches read per call, interleaved rounds.
+AB_N / AB_P set the mode set n <= N and the point count (default 60, 1e6).
 python tools/series_ab.py [VAR=a,b ...]   (default ZK_SERIES_SCALED=0,1)"""
 import os
 import sys
@@ -10,8 +11,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2409_19156_b200 as zb  # noqa: E402
 
-P = 1_000_000
-modes = zb.full_mode_set(60)
+P = int(os.environ.get("AB_P", 1_000_000))
+modes = zb.full_mode_set(int(os.environ.get("AB_N", 60)))
 M = len(modes)
 rng = np.random.default_rng(0)
 rho = torch.from_numpy(np.sqrt(rng.uniform(size=P))).cuda()
