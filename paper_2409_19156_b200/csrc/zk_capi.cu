@@ -302,11 +302,14 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
     // 4 points per thread for the plain radial k=0 basis, 2 when the thread also
     // carries the angular factors or derivative chains (register budget)
     int want = env_int("ZK_VEC", (K == 0 && theta == nullptr) ? 4 : 2);
-    // small requests: 2 points per thread when 4 would leave most SMs idle
-    // (config 1, 231 modes x 1e3 points: 8.3 -> 7.2 us)
+    // small requests: 2 points per thread when 4 would give fewer than ~2.7
+    // waves of 4-CTA-per-SM slots (config 1, 231 modes x 1e3 points: 8.3 ->
+    // 7.2 us; n = 50 x 2e4 points: 40.5 -> 36.1 us; a 1/8 shard of config 2,
+    // 12.5k points: 83.5 -> 80.9 us; config 4, 2,010 CTAs, stays at 4: 246
+    // vs 252 us)
     const int64_t groups = static_cast<int64_t>(plan->host.groups.size());
     if (want == 4 && std::getenv("ZK_VEC") == nullptr &&
-        (P + 1023) / 1024 * groups < 2 * int64_t(ctx->sm_count))
+        (P + 1023) / 1024 * groups < 11 * int64_t(ctx->sm_count))
       want = 2;
     for (int v : {4, 2}) {
       if (v <= want && fits(v)) {
