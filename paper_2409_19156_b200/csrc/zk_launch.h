@@ -72,9 +72,10 @@ size_t series_scratch_bytes(long long nrowslots);
 size_t series_fma_smem_bytes(int K, int max_jmax, int nc, bool exact);
 cudaError_t launch_series(const SeriesArgs& a, int K, int max_jmax, long long nrowslots,
                           double* rowc, bool dmma, cudaStream_t st, int* launches);
-// k = 0, one coefficient vector, whole plan resident in shared memory
-// (zk_series_k0.cu); cudaErrorNotSupported when the request does not qualify
-size_t series_k0_smem_bytes(long long nrows, int ngroups, int vec);
+// k = 0, 1..6 coefficient vectors (passes of 2 and 1), whole plan resident
+// in shared memory (zk_series_k0.cu); cudaErrorNotSupported when the request
+// does not qualify
+size_t series_k0_smem_bytes(long long nrows, int ngroups, int vec, int nc);
 cudaError_t launch_series_k0(const SeriesArgs& a, long long nrows, double* scratch, int vec,
                              cudaStream_t st, int* launches);
 int series_dmma_chunks(int ncoef);

@@ -1,12 +1,13 @@
-// K3, single coefficient vector, k = 0: f = B c for the 2-D (or radial) basis
-// with the whole plan resident in shared memory (config 5).
+// K3, k = 0, up to 6 coefficient vectors: f = B C for the 2-D (or radial)
+// basis with the whole plan resident in shared memory (
+// config 5). NC = 1 or 2 vectors per pass share the recursion.
 //
 // The general series kernel (zk_series.cu) stages each alpha group's tables
 // with a CTA barrier and parks the per-point group state in shared memory; at
 // config 5 (61 groups of ~16 keys) that per-group work was more instructions
 // than the keys themselves. This kernel removes it:
 //
-//  * one table of 32-byte key records {a', b', s C+, s C-} (row slot order,
+//  * one table of key records {a', b', (s C+, s C-) x NC} (row slot order,
 //    series_rec_kernel) plus the group records are loaded into shared memory
 //    ONCE per CTA by a bulk copy (cp.async.bulk, SASS UBLKCP) on an mbarrier;
 //    no per-group staging or barrier;
@@ -25,6 +26,8 @@
 // different rounding (tests/test_gpu_series.py measures it against binary128).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "zk_kernels.cuh"
 #include "zk_launch.h"
 
@@ -39,38 +42,54 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 }
 }  // namespace
 
-// rec[row0 + j] = {a'_j, b'_j, (-1)^j s_j C+_j, (-1)^j s_j C-_j} of chain 0 for
-// every key (alpha, j) of the plan (one CTA per group, a thread per degree)
-template <bool ANG>
+// rec[(row0 + j) RS ..] = {a'_j, b'_j, ((-1)^j s_j C+_j, (-1)^j s_j C-_j) for
+// vectors v0 .. v0+NC-1} of chain 0 for every key (alpha, j) of the plan, RS =
+// 2 + 2 NC doubles (vectors past ncoef are zero); one CTA per group, a thread
+// per degree
+template <bool ANG, int NC>
 __global__ void series_rec_kernel(const GroupRec* __restrict__ groups,
                                   const int32_t* __restrict__ rowptr,
                                   const int32_t* __restrict__ cols, const TolQ* __restrict__ tolq,
                                   const TolCoef* __restrict__ tol, const double* __restrict__ c,
-                                  double4* __restrict__ rec) {
+                                  long long ldc, int v0, int nc, double* __restrict__ rec) {
+  constexpr int RS = 2 + 2 * NC;
   const GroupRec g = groups[blockIdx.x];
   for (int j = threadIdx.x; j <= g.jmax; j += blockDim.x) {
-    double cp = 0.0, cn = 0.0;
+    double cp[NC], cn[NC];
+#pragma unroll
+    for (int v = 0; v < NC; ++v) cp[v] = cn[v] = 0.0;
     for (int r = rowptr[g.row0 + j]; r < rowptr[g.row0 + j + 1]; ++r) {
       const int code = cols[r];
-      const double x = c[code >> 1];
-      if (ANG && (code & 1)) cn += x; else cp += x;
+#pragma unroll
+      for (int v = 0; v < NC; ++v) {
+        if (v < nc) {
+          const double x = c[(code >> 1) + (v0 + v) * ldc];
+          if (ANG && (code & 1)) cn[v] += x; else cp[v] += x;
+        }
+      }
     }
     const double s = ((j & 1) ? -1.0 : 1.0) * tol[g.coef_off + j].s;
     const TolQ q = tolq[g.coef_off + j];
-    rec[g.row0 + j] = make_double4(q.a, q.b, s * cp, s * cn);
+    double2* dst = reinterpret_cast<double2*>(rec + static_cast<long long>(g.row0 + j) * RS);
+    dst[0] = make_double2(q.a, q.b);
+#pragma unroll
+    for (int v = 0; v < NC; ++v) dst[1 + v] = make_double2(s * cp[v], s * cn[v]);
   }
 }
 
 // One pass over the whole plan for V points per thread: points p0 .. p0+V-1
-// (those below pend). Per-point state in registers; the anchor state is
-// parked in shared memory (park[(f V + v) kT + tid]).
-template <bool ANG, int V>
+// (those below pend), NC coefficient vectors (output columns v0 ..). Per-point
+// state in registers; the anchor state is parked in shared memory
+// (park[(f V + v) kT + tid]).
+template <bool ANG, int V, int NC>
 __device__ __forceinline__ void k0_points(const SeriesArgs& a, const GroupRec* grp,
-                                          const double4* tab, double* park, long long p0,
-                                          long long pend, const unsigned long long* bar) {
+                                          const double* tab, double* park, long long p0,
+                                          long long pend, double* fout, int nc,
+                                          const unsigned long long* bar) {
+  constexpr int RS = 2 + 2 * NC;  // doubles per key record
   const int tid = threadIdx.x;
   auto pk = [&](int f, int v) -> double& { return park[(f * V + v) * kT + tid]; };
-  double u[V], zr[V], zi[V], wr[V], wi[V], acc[V];
+  double u[V], zr[V], zi[V], wr[V], wi[V], acc[NC][V];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const bool live = p0 + v < pend;
@@ -88,7 +107,8 @@ __device__ __forceinline__ void k0_points(const SeriesArgs& a, const GroupRec* g
     }
     wr[v] = 1.0;
     wi[v] = 0.0;
-    acc[v] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c][v] = 0.0;
     pk(0, v) = r;
     pk(1, v) = t;
     pk(2, v) = 1.0;
@@ -151,70 +171,91 @@ __device__ __forceinline__ void k0_points(const SeriesArgs& a, const GroupRec* g
 
     // the group's keys: X = sum Q C+, Y = sum Q C-; degrees 0 and 1 peeled
     // (Q_0 = 1, Q_1 = a'_1 x + b'_1)
-    const double4* R = tab + g.row0;
+    const double* R = tab + g.row0 * RS;  // int offsets keep the address uniform
     const int jmax = g.jmax;
-    double gx[V], gy[V], q1[V], q0[V];
-    {
-      const double2 c0 = *reinterpret_cast<const double2*>(&R[0].z);
-      if (jmax >= 1) {
-        const double2 ab = *reinterpret_cast<const double2*>(&R[1].x);
-        const double2 cc = *reinterpret_cast<const double2*>(&R[1].z);
+    double gx[NC][V], gy[NC][V], q1[V], q0[V];
+    if (jmax >= 1) {
+      const double2 ab = *reinterpret_cast<const double2*>(R + RS);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        q0[v] = 1.0;
+        q1[v] = fma(ab.x, u[v], ab.y);
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double2 c0 = *reinterpret_cast<const double2*>(R + 2 + 2 * c);
+        const double2 c1 = *reinterpret_cast<const double2*>(R + RS + 2 + 2 * c);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          q0[v] = 1.0;
-          q1[v] = fma(ab.x, u[v], ab.y);
-          gx[v] = fma(q1[v], cc.x, c0.x);
-          gy[v] = fma(q1[v], cc.y, c0.y);
-        }
-      } else {
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          gx[v] = c0.x;
-          gy[v] = c0.y;
-          q1[v] = q0[v] = 0.0;
+          gx[c][v] = fma(q1[v], c1.x, c0.x);
+          gy[c][v] = fma(q1[v], c1.y, c0.y);
         }
       }
+    } else {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double2 c0 = *reinterpret_cast<const double2*>(R + 2 + 2 * c);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          gx[c][v] = c0.x;
+          gy[c][v] = c0.y;
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) q1[v] = q0[v] = 0.0;
     }
 #pragma unroll 4
     for (int j = 2; j <= jmax; ++j) {
-      const double2 ab = *reinterpret_cast<const double2*>(&R[j].x);
-      const double2 cc = *reinterpret_cast<const double2*>(&R[j].z);
+      const double* Rj = R + j * RS;
+      const double2 ab = *reinterpret_cast<const double2*>(Rj);
+      double2 cc[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) cc[c] = *reinterpret_cast<const double2*>(Rj + 2 + 2 * c);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const double qn = fma(fma(ab.x, u[v], ab.y), q1[v], -q0[v]);
         q0[v] = q1[v];
         q1[v] = qn;
-        gx[v] = fma(qn, cc.x, gx[v]);
-        if (ANG) gy[v] = fma(qn, cc.y, gy[v]);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          gx[c][v] = fma(qn, cc[c].x, gx[c][v]);
+          if (ANG) gy[c][v] = fma(qn, cc[c].y, gy[c][v]);
+        }
       }
     }
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      acc[v] = fma(gx[v], wr[v], acc[v]);
-      if (ANG) acc[v] = fma(gy[v], wi[v], acc[v]);
-    }
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        acc[c][v] = fma(gx[c][v], wr[v], acc[c][v]);
+        if (ANG) acc[c][v] = fma(gy[c][v], wi[v], acc[c][v]);
+      }
   }
 #pragma unroll
-  for (int v = 0; v < V; ++v)
-    if (p0 + v < pend) a.f[p0 + v] = acc[v];
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (p0 + v < pend && (NC == 1 || c < nc)) fout[p0 + v + c * a.ldf] = acc[c][v];
 }
 
-// One CTA per tile of kT x VEC points (VEC 3: 2.9 waves of 444 CTA slots at
-// config 5). Measured and not kept: persistent CTAs over equal contiguous
-// shares walked in passes of 4 points per thread plus a 2-point remainder
-// pass (0.447 vs 0.413 ms), and 4 points per thread in 3.3 waves (0.416).
-template <bool ANG, int VEC>
+// One CTA per tile of kT x VEC points (VEC 3, one vector: 2.9 waves of 444
+// CTA slots at config 5). Measured and not kept: persistent CTAs over equal
+// contiguous shares walked in passes of 4 points per thread plus a 2-point
+// remainder pass (0.447 vs 0.413 ms), and 4 points per thread in 3.3 waves
+// (0.416).
+template <bool ANG, int VEC, int NC>
 __global__ void __launch_bounds__(kT, VEC >= 4 ? 2 : 3)
-series_k0_kernel(const SeriesArgs a, const double4* __restrict__ rec, int nrows) {
+series_k0_kernel(const SeriesArgs a, const double* __restrict__ rec, int nrows, int v0, int nc) {
+  constexpr int RS = 2 + 2 * NC;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long bar;
   const int tid = threadIdx.x;
   double* park = sm;
-  const double4* tab = reinterpret_cast<const double4*>(sm + kPark0 * VEC * kT);
-  const GroupRec* grp = reinterpret_cast<const GroupRec*>(tab + nrows);
+  const double* tab = sm + kPark0 * VEC * kT;
+  const GroupRec* grp = reinterpret_cast<const GroupRec*>(tab + static_cast<long long>(nrows) * RS);
 
   // the key records and group records: one bulk copy each, one mbarrier
-  const unsigned tab_bytes = static_cast<unsigned>(nrows) * 32u;
+  const unsigned tab_bytes = static_cast<unsigned>(nrows) * RS * 8u;
   const unsigned grp_bytes = static_cast<unsigned>(a.ngroups) * 32u;
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
@@ -237,20 +278,24 @@ series_k0_kernel(const SeriesArgs a, const double4* __restrict__ rec, int nrows)
   }
   const long long ntiles = (a.P + kT * VEC - 1) / (kT * VEC);
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-    k0_points<ANG, VEC>(a, grp, tab, park, tile * (kT * VEC) + tid * VEC, a.P,
-                        tile == blockIdx.x ? &bar : nullptr);
+    k0_points<ANG, VEC, NC>(a, grp, tab, park, tile * (kT * VEC) + tid * VEC, a.P,
+                            a.f + static_cast<long long>(v0) * a.ldf, nc,
+                            tile == blockIdx.x ? &bar : nullptr);
 }
 
-size_t series_k0_smem_bytes(long long nrows, int ngroups, int vec) {
-  return size_t(kPark0) * vec * kT * sizeof(double) + size_t(nrows) * 32 + size_t(ngroups) * 32;
+size_t series_k0_smem_bytes(long long nrows, int ngroups, int vec, int nc) {
+  return size_t(kPark0) * vec * kT * sizeof(double) + size_t(nrows) * (2 + 2 * nc) * 8 +
+         size_t(ngroups) * 32;
 }
 
-// the kernel for (ANG, VEC), its shared memory attribute set; nullptr when
+using K0Fn = void (*)(const SeriesArgs, const double*, int, int, int);
+
+// the kernel for (ANG, VEC, NC), its shared memory attribute set; nullptr when
 // fewer than 2 CTAs fit an SM (large tables: the staged kernel is faster,
 // measured n = 120: 1.68 vs 1.55 ms at 1e6 points; n = 100 at 2 CTAs: 0.99 vs 1.14)
-template <bool ANG, int VEC>
-static void (*k0_kernel_for(size_t smem))(const SeriesArgs, const double4*, int) {
-  auto fn = series_k0_kernel<ANG, VEC>;
+template <bool ANG, int VEC, int NC>
+static K0Fn k0_kernel_for(size_t smem) {
+  K0Fn fn = series_k0_kernel<ANG, VEC, NC>;
   int per_sm = 0;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem)) != cudaSuccess ||
@@ -261,33 +306,72 @@ static void (*k0_kernel_for(size_t smem))(const SeriesArgs, const double4*, int)
   return per_sm >= 2 ? fn : nullptr;
 }
 
+template <bool ANG>
+static K0Fn k0_select(int vec, int nc, size_t smem) {
+  if (nc == 2) return k0_kernel_for<ANG, 2, 2>(smem);
+  return vec == 2   ? k0_kernel_for<ANG, 2, 1>(smem)
+         : vec == 4 ? k0_kernel_for<ANG, 4, 1>(smem)
+                    : k0_kernel_for<ANG, 3, 1>(smem);
+}
+
+// Passes of NC = 2 or 1 vectors (3 vectors: 2 + 1), each a record kernel + the
+// resident kernel, for up to 6 vectors (ZK_SERIES_K0_MAXV). Config 5
+// (`tools/series_ab.py`, AB_V = V): V = 1 / 2 / 3 / 4 / 6 / 8 take 0.40 / 0.55 /
+// 0.92 / 1.08 / 1.61 / 2.14 ms vs 0.51 / 0.72 / 1.13 / 1.14 / 1.95 / 1.96 staged
+// (NC up to 8), so 7-8 vectors stay staged; a 4-wide resident pass (128
+// registers) measured 2.16 ms at V = 4. cudaErrorNotSupported (before any
+// launch) when a request does not qualify or a pass's table does not leave 2
+// CTAs per SM.
 cudaError_t launch_series_k0(const SeriesArgs& a, long long nrows, double* scratch, int vec,
                              cudaStream_t st, int* launches) {
-  const size_t smem = series_k0_smem_bytes(nrows, a.ngroups, vec);
-  if (a.ncoef != 1 || a.exact || !a.tolq || smem > size_t(a.max_smem))
+  static const int maxv = [] {
+    const char* v = std::getenv("ZK_SERIES_K0_MAXV");
+    return v && *v ? std::atoi(v) : 6;
+  }();
+  if (a.ncoef < 1 || a.ncoef > maxv || a.ncoef > 8 || a.exact || !a.tolq)
     return cudaErrorNotSupported;
-  void (*fn)(const SeriesArgs, const double4*, int) =
-      a.theta ? (vec == 2 ? k0_kernel_for<true, 2>(smem)
-                 : vec == 4 ? k0_kernel_for<true, 4>(smem) : k0_kernel_for<true, 3>(smem))
-              : (vec == 2 ? k0_kernel_for<false, 2>(smem)
-                 : vec == 4 ? k0_kernel_for<false, 4>(smem) : k0_kernel_for<false, 3>(smem));
-  if (!fn) return cudaErrorNotSupported;
+  struct Pass {
+    int v0, nc, take;
+    K0Fn fn;
+    size_t smem;
+  };
+  Pass passes[8];
+  int np = 0;
+  for (int v0 = 0; v0 < a.ncoef;) {
+    const int left = a.ncoef - v0;
+    const int nc = left >= 2 ? 2 : 1;
+    const int v = nc == 1 ? (vec == 2 || vec == 4 ? vec : 3) : 2;
+    const size_t smem = series_k0_smem_bytes(nrows, a.ngroups, v, nc);
+    if (smem > size_t(a.max_smem)) return cudaErrorNotSupported;
+    const K0Fn fn = a.theta ? k0_select<true>(v, nc, smem) : k0_select<false>(v, nc, smem);
+    if (!fn) return cudaErrorNotSupported;
+    const int take = left < nc ? left : nc;
+    passes[np++] = Pass{v0, nc, take, fn, smem};
+    v0 += take;
+  }
   if (a.P <= 0) return cudaSuccess;
-  double4* rec = reinterpret_cast<double4*>(scratch);
-  if (a.theta)
-    series_rec_kernel<true><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.tolq, a.tol,
-                                                       a.c, rec);
-  else
-    series_rec_kernel<false><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.tolq, a.tol,
-                                                        a.c, rec);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  const int v = vec == 2 || vec == 4 ? vec : 3;
-  const long long ntiles = (a.P + kT * v - 1) / (kT * v);
-  fn<<<static_cast<unsigned>(ntiles), kT, smem, st>>>(a, rec, static_cast<int>(nrows));
-  e = cudaGetLastError();
-  if (e == cudaSuccess) *launches += 2;
-  return e;
+  for (int i = 0; i < np; ++i) {
+    const Pass& q = passes[i];
+    const int v = q.nc == 1 ? (vec == 2 || vec == 4 ? vec : 3) : 2;
+#define ZK_REC(ANGV, NCV)                                                                      \
+  series_rec_kernel<ANGV, NCV><<<a.ngroups, 128, 0, st>>>(a.groups, a.rowptr, a.cols, a.tolq, \
+                                                          a.tol, a.c, a.ldc, q.v0, q.take, scratch)
+    if (a.theta) {
+      if (q.nc == 2) ZK_REC(true, 2); else ZK_REC(true, 1);
+    } else {
+      if (q.nc == 2) ZK_REC(false, 2); else ZK_REC(false, 1);
+    }
+#undef ZK_REC
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const long long ntiles = (a.P + kT * v - 1) / (kT * v);
+    q.fn<<<static_cast<unsigned>(ntiles), kT, q.smem, st>>>(a, scratch, static_cast<int>(nrows),
+                                                            q.v0, q.take);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    *launches += 2;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace zk

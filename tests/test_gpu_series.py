@@ -144,6 +144,25 @@ ENGINES = {  # single-vector k = 0 series engines (environment switches read per
 }
 
 
+@pytest.mark.parametrize("V", [2, 3, 5, 6, 7])
+def test_series_resident_multi_vector_passes(monkeypatch, V):
+    """Several vectors on the resident kernel (passes of 2 and 1 vectors, up to
+    6) and on the staged kernel (7+): every column against B @ C, 2-D and
+    radial, with a point count that is not a tile multiple."""
+    modes = zb.full_mode_set(17)
+    pairs = [(md.n, md.m) for md in modes]
+    rho, theta = disc(1237, V)
+    C = np.random.default_rng(V).standard_normal((len(modes), V))
+    for engine in ("3", "0"):
+        monkeypatch.setenv("ZK_SERIES_K0", engine)
+        for th in (theta, None):
+            f = zb.series_eval(modes, C, rho, th)
+            B = orc.basis_2d(pairs, rho, theta) if th is not None else orc.radial_batch(pairs, rho, 0)
+            scale = np.abs(B) @ np.abs(C)
+            assert f.shape == (1237, V)
+            assert (np.abs(f - B @ C) <= 1e-13 * scale + 1e-300).all(), (V, engine, th is None)
+
+
 @pytest.mark.parametrize("engine", sorted(ENGINES))
 def test_series_k0_engines_edge_cases(monkeypatch, engine):
     """Every single-vector k = 0 engine against B @ c of the oracle: the

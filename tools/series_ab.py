@@ -1,6 +1,7 @@
 """A/B timing of the config-5 series (one coefficient vector, device-resident,
 CUDA events) under environment switches read per call, interleaved rounds.
-AB_N / AB_P set the mode set n <= N and the point count (default 60, 1e6).
+AB_N / AB_P / AB_V set the mode set n <= N, the point count and the number of
+coefficient vectors (default 60, 1e6, 1).
 python tools/series_ab.py [VAR=a,b ...]   (default ZK_SERIES_SCALED=0,1)"""
 import os
 import sys
@@ -17,7 +18,9 @@ M = len(modes)
 rng = np.random.default_rng(0)
 rho = torch.from_numpy(np.sqrt(rng.uniform(size=P))).cuda()
 th = torch.from_numpy(2 * np.pi * rng.uniform(size=P)).cuda()
-c = torch.from_numpy(rng.standard_normal(M)).cuda()
+NV = int(os.environ.get("AB_V", 1))  # coefficient vectors
+c = torch.from_numpy(rng.standard_normal(M) if NV == 1 else
+                     np.asfortranarray(rng.standard_normal((M, NV)))).cuda()
 specs = sys.argv[1:] or ["ZK_SERIES_SCALED=0,1"]
 arms = [("", "")]
 for s in specs:
