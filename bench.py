@@ -329,7 +329,19 @@ def run_c5fit(args, world, rank, local, dist, stream, comm):
     coef = torch.from_numpy(coef_h).to(dev)
     G = torch.zeros((M, M), dtype=torch.float64, device=dev)
     r = torch.zeros(M, dtype=torch.float64, device=dev)
+    y = torch.empty(hi - lo, dtype=torch.float64, device=dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    # K3 through the C ABI on preallocated buffers (the phase is device time,
+    # not the Python wrapper's argument handling)
+    n_arr, m_arr = zb.modes.mode_arrays(modes)
+    sctx = zb._lib.context(local)
+    splan = zb._lib.plan_for(sctx, n_arr, m_arr)
+
+    def series_k3():
+        sctx.set_stream(stream.cuda_stream)
+        zb._lib.check(zb._lib.lib.zk_series_eval(
+            sctx.handle, splan.handle, rho.data_ptr(), th.data_ptr(), hi - lo, 0,
+            coef.data_ptr(), 1, M, y.data_ptr(), hi - lo, zb._lib.ZK_ASYNC), "zk_series_eval")
     phase = np.zeros(4)
     x = None
 
@@ -337,7 +349,7 @@ def run_c5fit(args, world, rank, local, dist, stream, comm):
         nonlocal x
         if record:
             ev[0].record(stream)
-        y = zs.series_device(modes, coef, rho, th)                  # K3
+        series_k3()                                                  # K3
         if record:
             ev[1].record(stream)
         G.zero_()
