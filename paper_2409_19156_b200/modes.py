@@ -78,7 +78,14 @@ def make_mode(n: int, m: int) -> Mode:
 
 
 def as_mode_set(pairs: Iterable) -> ModeSet:
-    """zk/modes.py:67-76: Mode instances pass through, pairs are validated."""
+    """zk/modes.py:67-76: Mode instances pass through, pairs are validated.
+    A tuple of Modes (an immutable ModeSet) is returned as is, so the per-set
+    memo (mode_set_entry) keeps hitting across calls with the same set."""
+    if isinstance(pairs, tuple):
+        with _SET_CACHE_LOCK:
+            hit = _SET_CACHE.get(id(pairs))
+        if (hit is not None and hit[0] is pairs) or all(isinstance(p, Mode) for p in pairs):
+            return pairs
     return tuple(p if isinstance(p, Mode) else make_mode(*p) for p in pairs)
 
 
