@@ -211,7 +211,7 @@ int ensure_chunk_events(zk_ctx* ctx, size_t n) {
 }
 
 struct Geometry {
-  int vec, ntiles, nchunks, tiles_per_chunk, grid, col_cap, stage_slots;
+  int vec, threads, ntiles, nchunks, tiles_per_chunk, grid, col_cap, stage_slots;
   bool tma;
   size_t smem;
 };
@@ -253,10 +253,11 @@ void column_copy(double* dst, const double* src, size_t n) {
 
 
 Geometry geometry(const zk_ctx* ctx, const zk_plan* plan, int64_t P, int K, bool all, int vec,
-                  bool tma, bool coef_global = false) {
+                  bool tma, bool coef_global, int threads) {
   Geometry g{};
   g.vec = vec;
-  const int64_t tile_pts = int64_t(zk::kRadialThreads) * g.vec;
+  g.threads = threads;
+  const int64_t tile_pts = int64_t(threads) * g.vec;
   g.ntiles = static_cast<int>((P + tile_pts - 1) / tile_pts);
   const int64_t G = static_cast<int64_t>(plan->host.groups.size());
   // one tile per CTA for the store-bound orders; the FP64-bound single-order
@@ -319,14 +320,17 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
     }
   }
   const bool tma = !force_scalar && !exact_pow && vec >= 2 && env_int("ZK_TMA", 0) != 0;
-  Geometry geo = geometry(ctx, plan, P, K, all, vec, tma);
+  const bool ang = theta != nullptr;
+  Geometry geo = geometry(ctx, plan, P, K, all, vec, tma, false,
+                          zk::radial_threads(K, all, ang, vec, tma, false, exact_pow));
   bool coef_global = false;
   if (geo.smem > ctx->max_smem) {
     // very long chains: coefficient tables stay in global memory (scalar-store
     // fallback kernel); only the column offsets and row pointers are staged
     coef_global = true;
     vec = 1;
-    geo = geometry(ctx, plan, P, K, all, vec, false, true);
+    geo = geometry(ctx, plan, P, K, all, vec, false, true,
+                   zk::radial_threads(K, all, ang, vec, false, true, exact_pow));
   }
   if (geo.smem > ctx->max_smem)
     return fail(ZK_EINVAL, "mode set too large for the shared-memory column stage "
@@ -351,6 +355,7 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
   a.stage_slots = geo.stage_slots;
   a.coef_global = coef_global ? 1 : 0;
   a.exact_pow = exact_pow ? 1 : 0;
+  a.threads = geo.tma ? zk::kRadialThreads : geo.threads;
   cudaError_t e = zk::launch_radial(a, K, all, theta != nullptr, geo.vec, geo.tma, geo.grid, geo.smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "radial kernel launch");
   ctx->launches += 1;

@@ -10,6 +10,7 @@
 namespace zk {
 
 constexpr int kRadialThreads = 256;
+constexpr int kRadialThreadsSmall = 128;  // single-order k >= 2 (radial_threads)
 
 struct RadialArgs {
   const GroupRec* groups;
@@ -33,9 +34,14 @@ struct RadialArgs {
                           //    (L1-cached broadcasts) instead of staging them in smem
   int exact_pow;          // 1: every rho power correctly rounded at any rho (VEC = 1
                           //    kernels, make_powset_exact; ZK_EXACT_POW)
+  int threads;            // CTA size of the launch (radial_threads)
 };
 
 int radial_stages(bool all);
+// CTA size of a K1/K2 launch: 128 for single-order k >= 2 radial requests at 2
+// points per thread (ZK_SMALL_CTA=0 disables), 256 otherwise
+int radial_threads(int K, bool all, bool ang, int vec, bool tma, bool coef_global,
+                   bool exact_pow);
 size_t radial_smem_bytes(int K, bool all, int vec, bool tma, int stage_slots, int max_jmax,
                          int col_cap, bool coef_global = false);
 cudaError_t launch_radial(const RadialArgs& a, int K, bool all, bool ang, int vec, bool tma,

@@ -167,12 +167,14 @@ struct Thread {
 
 // EXACTP: the opt-in exact-power mode -- every rho power RN(rho^e) at any rho
 // (make_powset_exact: exponent carried apart, subnormal results rounded once)
-template <int K, bool ALL, bool ANG, int VEC, bool TMA, bool GC = false, bool EXACTP = false>
+template <int K, bool ALL, bool ANG, int VEC, bool TMA, bool GC = false, bool EXACTP = false,
+          int NT = kRadialThreads>
 __device__ __forceinline__ void radial_basis_body(const RadialArgs& a) {
+  static_assert(NT == kRadialThreads || !TMA, "the TMA store ring assumes kRadialThreads");
   using T = Thread<K, ALL, ANG, VEC>;
   constexpr int NO = T::NO;
   constexpr int S = kRingStages;
-  constexpr int TP = kRadialThreads * VEC;  // points per tile
+  constexpr int TP = NT * VEC;  // points per tile
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int slot = blockIdx.x / a.nchunks;
   const int chunk = blockIdx.x - slot * a.nchunks;
@@ -464,6 +466,16 @@ radial_basis_kernel_2cta(const RadialArgs a) {
   radial_basis_body<K, ALL, ANG, VEC, TMA>(a);
 }
 
+// Single-order k >= 2 in 128-thread CTAs: twice the CTAs of the same register
+// budget, so an SM's warps come from more, independent CTAs (their staging and
+// tile boundaries desynchronise). Config 3 k = 3: 0.779 vs 0.815 ms (k = 2
+// unchanged; the store-bound kernels stay at 256: all orders 2.44 vs 2.39).
+template <int K, int VEC>
+__global__ void __launch_bounds__(kRadialThreadsSmall)
+radial_basis_kernel_small(const RadialArgs a) {
+  radial_basis_body<K, false, false, VEC, false, false, false, kRadialThreadsSmall>(a);
+}
+
 // Three CTAs per SM (<= 85 registers): kept for the ZK_MINB=3 experiment
 // (spills for k >= 2 on this build; see launch_t).
 template <int K, bool ALL, bool ANG, int VEC, bool TMA>
@@ -495,6 +507,8 @@ static cudaError_t launch_t(const RadialArgs& a, int grid, size_t smem, cudaStre
     fn = b == 3   ? radial_basis_kernel_3cta<K, ALL, ANG, VEC, TMA>
          : b == 2 ? radial_basis_kernel_2cta<K, ALL, ANG, VEC, TMA>
                   : radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
+    if constexpr (!ANG)
+      if (a.threads == kRadialThreadsSmall) fn = radial_basis_kernel_small<K, VEC>;
   } else {
     fn = radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
   }
@@ -503,7 +517,7 @@ static cudaError_t launch_t(const RadialArgs& a, int grid, size_t smem, cudaStre
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  fn<<<grid, kRadialThreads + (TMA ? 32 : 0), smem, st>>>(a);
+  fn<<<grid, (TMA ? kRadialThreads + 32 : a.threads), smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -557,6 +571,17 @@ static cudaError_t launch_k(const RadialArgs& a, bool all, bool ang, int vec, bo
 }
 
 int radial_stages(bool) { return kRingStages; }
+
+int radial_threads(int K, bool all, bool ang, int vec, bool tma, bool coef_global,
+                   bool exact_pow) {
+  static const int small = [] {
+    const char* v = std::getenv("ZK_SMALL_CTA");
+    return v && *v ? std::atoi(v) : 1;
+  }();
+  return (small && K >= 2 && !all && !ang && vec == 2 && !tma && !coef_global && !exact_pow)
+             ? kRadialThreadsSmall
+             : kRadialThreads;
+}
 
 size_t radial_smem_bytes(int K, bool all, int vec, bool tma, int stage_slots, int max_jmax,
                          int col_cap, bool coef_global) {
