@@ -44,7 +44,10 @@
 // rho^alpha, cos/sin of theta and of alpha*theta) is parked in shared memory
 // while the key loop runs, and the k = 0 single-vector kernel carries 3
 // points per thread (each per-key coefficient load serves 3 points; 1e6
-// points fill 2.9 waves). Config 5: 0.88 (round 1) -> 0.52 ms.
+// points fill 2.9 waves). Config 5: 0.88 (round 1) -> 0.52 ms here; k = 0
+// requests of up to 6 vectors whose plan fits shared memory twice per SM now
+// run the resident kernel instead (zk_series_k0.cu: 0.40 ms), this one takes
+// k > 0, larger plans and 7-8 vectors (k = 0 on the scaled chains, kTolQ).
 #include <cuda_runtime.h>
 
 #include <type_traits>
