@@ -1,9 +1,10 @@
 #!/bin/bash
-# usage: tools/gram_cmp.sh P [extra env for the second run...]: bitwise compare of the Gram
-# (tools/gram_save.py) between the default build and ZK_GRAM_TMA=1
-P=$1
+# usage: tools/gram_cmp.sh [P]: bitwise compare of the Gram (tools/gram_save.py) between
+# the default TMA operand path and the cp.async ring (ZK_GRAM_TMA=0); P defaults to 2e5
+P=${1:-200000}
+mkdir -p gpurun_out
 python tools/gram_save.py gpurun_out/ga.npy $P
-ZK_GRAM_TMA=1 python tools/gram_save.py gpurun_out/gb.npy $P
+ZK_GRAM_TMA=0 python tools/gram_save.py gpurun_out/gb.npy $P
 python - <<PY
 import numpy as np
 a = np.load("gpurun_out/ga.npy"); b = np.load("gpurun_out/gb.npy"); M = 1891
