@@ -501,6 +501,35 @@ def test_store_paths_agree_bitwise(monkeypatch, vec):
     assert within_tolerance(base[3].values[:64], ref)
 
 
+def test_single_order_cta_sizes_agree_bitwise(tmp_path):
+    """Single-order k >= 2 requests run 128-thread CTAs by default and 256-thread
+    ones with ZK_SMALL_CTA=0 (read once per process, hence subprocesses): same
+    bits, partial tiles included, and within tolerance of the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1]); "
+        "import paper_2409_19156_b200 as zb; "
+        "modes = zb.full_mode_set(45); "
+        "grid = np.random.default_rng(21).uniform(size=3001); "
+        "out = [zb.evaluate_batch(zb.BatchRequest(modes=modes, grid=grid, deriv_order=k))[0].values "
+        "for k in (2, 3)]; np.save(sys.argv[2], np.stack(out))")
+    outs = []
+    for flag in ("1", "0"):
+        path = tmp_path / f"cta{flag}.npy"
+        subprocess.run([sys.executable, "-c", code, root, str(path)], check=True, timeout=600,
+                       env=dict(os.environ, ZK_SMALL_CTA=flag), cwd=root)
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
+    modes = zb.full_mode_set(45)
+    grid = np.random.default_rng(21).uniform(size=3001)
+    for i, k in enumerate((2, 3)):
+        ref = orc.radial_batch(pairs(modes), grid[:50], k)
+        assert within_tolerance(outs[0][i][:50], ref)
+
+
 def test_parallel_shards_over_devices_bitwise(monkeypatch):
     """parallel=True splits the points across devices (here: two shards on
     the one available GPU via ZK_DEVICES=0,0); every shard writes its rows of
