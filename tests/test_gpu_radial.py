@@ -504,7 +504,9 @@ def test_store_paths_agree_bitwise(monkeypatch, vec):
 def test_single_order_cta_sizes_agree_bitwise(tmp_path):
     """Single-order k >= 2 requests run 128-thread CTAs by default and 256-thread
     ones with ZK_SMALL_CTA=0 (read once per process, hence subprocesses): same
-    bits, partial tiles included, and within tolerance of the oracle."""
+    bits, partial tiles included (3,000 points: an even leading dimension keeps
+    2 points per thread, the small-CTA condition), and within tolerance of the
+    oracle."""
     import os
     import subprocess
     import sys
@@ -513,7 +515,7 @@ def test_single_order_cta_sizes_agree_bitwise(tmp_path):
         "import sys, numpy as np; sys.path.insert(0, sys.argv[1]); "
         "import paper_2409_19156_b200 as zb; "
         "modes = zb.full_mode_set(45); "
-        "grid = np.random.default_rng(21).uniform(size=3001); "
+        "grid = np.random.default_rng(21).uniform(size=3000); "
         "out = [zb.evaluate_batch(zb.BatchRequest(modes=modes, grid=grid, deriv_order=k))[0].values "
         "for k in (2, 3)]; np.save(sys.argv[2], np.stack(out))")
     outs = []
@@ -524,7 +526,7 @@ def test_single_order_cta_sizes_agree_bitwise(tmp_path):
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
     modes = zb.full_mode_set(45)
-    grid = np.random.default_rng(21).uniform(size=3001)
+    grid = np.random.default_rng(21).uniform(size=3000)
     for i, k in enumerate((2, 3)):
         ref = orc.radial_batch(pairs(modes), grid[:50], k)
         assert within_tolerance(outs[0][i][:50], ref)
