@@ -300,9 +300,9 @@ int launch_device(zk_ctx* ctx, const zk_plan* plan, const double* rho, const dou
   exact_pow = exact_pow || env_int("ZK_EXACT_POW", 0) != 0;
   int vec = 1;
   if (!force_scalar && !exact_pow) {
-    // 4 points per thread for the plain radial k=0 basis, 2 when the thread also
-    // carries the angular factors or derivative chains (register budget)
-    int want = env_int("ZK_VEC", (K == 0 && theta == nullptr) ? 4 : 2);
+    // 4 points per thread for the k=0 bases (the 2-D one in 128-thread CTAs,
+    // radial_threads), 2 when the thread carries derivative chains
+    int want = env_int("ZK_VEC", K == 0 ? 4 : 2);
     // small requests: 2 points per thread when 4 would give fewer than ~2.7
     // waves of 4-CTA-per-SM slots (config 1, 231 modes x 1e3 points: 8.3 ->
     // 7.2 us; n = 50 x 2e4 points: 40.5 -> 36.1 us; a 1/8 shard of config 2,

@@ -39,7 +39,8 @@ struct RadialArgs {
 
 int radial_stages(bool all);
 // CTA size of a K1/K2 launch: 128 for single-order k >= 2 radial requests at 2
-// points per thread (ZK_SMALL_CTA=0 disables), 256 otherwise
+// points per thread and the 2-D k = 0 basis at 4 (ZK_SMALL_CTA=0 disables),
+// 256 otherwise
 int radial_threads(int K, bool all, bool ang, int vec, bool tma, bool coef_global,
                    bool exact_pow);
 size_t radial_smem_bytes(int K, bool all, int vec, bool tma, int stage_slots, int max_jmax,

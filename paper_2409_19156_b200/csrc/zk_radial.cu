@@ -470,10 +470,13 @@ radial_basis_kernel_2cta(const RadialArgs a) {
 // budget, so an SM's warps come from more, independent CTAs (their staging and
 // tile boundaries desynchronise). Config 3 k = 3: 0.779 vs 0.815 ms (k = 2
 // unchanged; the store-bound kernels stay at 256: all orders 2.44 vs 2.39).
-template <int K, int VEC>
+// The 2-D k = 0 basis at 4 points per thread (94 registers) likewise: five
+// 128-thread CTAs per SM, 32-byte stores -- config 5 2.29 vs 2.33 ms at 2
+// points per thread in 256-thread CTAs (4 points at 256 threads: 2.39).
+template <int K, bool ANG, int VEC>
 __global__ void __launch_bounds__(kRadialThreadsSmall)
 radial_basis_kernel_small(const RadialArgs a) {
-  radial_basis_body<K, false, false, VEC, false, false, false, kRadialThreadsSmall>(a);
+  radial_basis_body<K, false, ANG, VEC, false, false, false, kRadialThreadsSmall>(a);
 }
 
 // Three CTAs per SM (<= 85 registers): kept for the ZK_MINB=3 experiment
@@ -508,9 +511,11 @@ static cudaError_t launch_t(const RadialArgs& a, int grid, size_t smem, cudaStre
          : b == 2 ? radial_basis_kernel_2cta<K, ALL, ANG, VEC, TMA>
                   : radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
     if constexpr (!ANG)
-      if (a.threads == kRadialThreadsSmall) fn = radial_basis_kernel_small<K, VEC>;
+      if (a.threads == kRadialThreadsSmall) fn = radial_basis_kernel_small<K, false, VEC>;
   } else {
     fn = radial_basis_kernel<K, ALL, ANG, VEC, TMA>;
+    if constexpr (K == 0 && ANG && VEC == 4 && !TMA)
+      if (a.threads == kRadialThreadsSmall) fn = radial_basis_kernel_small<K, true, VEC>;
   }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -578,7 +583,9 @@ int radial_threads(int K, bool all, bool ang, int vec, bool tma, bool coef_globa
     const char* v = std::getenv("ZK_SMALL_CTA");
     return v && *v ? std::atoi(v) : 1;
   }();
-  return (small && K >= 2 && !all && !ang && vec == 2 && !tma && !coef_global && !exact_pow)
+  const bool fp64_bound = K >= 2 && !all && !ang && vec == 2;
+  const bool basis_2d = K == 0 && ang && vec == 4;
+  return (small && (fp64_bound || basis_2d) && !tma && !coef_global && !exact_pow)
              ? kRadialThreadsSmall
              : kRadialThreads;
 }
