@@ -324,3 +324,29 @@ def test_release_buffers_then_recompute():
     zb.release_buffers()
     b, _ = zb.evaluate_batch(zb.BatchRequest(modes=modes, grid=grid))
     assert np.array_equal(b.values, av)
+
+
+def test_series_and_gram_empty_and_single_mode_edges():
+    """Degenerate shapes through the numpy API: no points (f has shape (0,) /
+    (0, V), G = 0), one mode (M = 1, the Gram's 1 x 1 block inside a 64-wide
+    tile), and a single point."""
+    modes = zb.full_mode_set(6)
+    M = len(modes)
+    f = zb.series_eval(modes, np.ones((M, 3)), np.zeros(0), np.zeros(0))
+    assert f.shape == (0, 3)
+    G, r = zb.gram(modes, np.zeros(0), np.zeros(0), np.zeros(0))
+    assert G.shape == (M, M) and not np.any(np.asarray(G.cpu() if hasattr(G, "cpu") else G))
+    one = zb.as_mode_set([(4, -2)])
+    rho, theta = disc(301, 77)
+    B = orc.basis_2d([(4, -2)], rho, theta)
+    f = zb.series_eval(one, np.array([2.5]), rho, theta)
+    assert np.abs(f - 2.5 * B[:, 0]).max() <= 1e-13
+    G, r = zb.gram(one, rho, theta, f)
+    G = np.asarray(G.cpu() if hasattr(G, "cpu") else G)
+    r = np.asarray(r.cpu() if hasattr(r, "cpu") else r)
+    assert abs(G[0, 0] - B[:, 0] @ B[:, 0]) <= 1e-12 * (B[:, 0] @ B[:, 0])
+    assert abs(r[0] - B[:, 0] @ f) <= 1e-12 * abs(B[:, 0]) @ abs(f)
+    rho1, theta1 = disc(1, 5)
+    f1 = zb.series_eval(modes, np.arange(M, dtype=float), rho1, theta1)
+    B1 = orc.basis_2d([(md.n, md.m) for md in modes], rho1, theta1)
+    assert np.abs(f1 - B1 @ np.arange(M)).max() <= 1e-12 * np.abs(B1).sum() * M
