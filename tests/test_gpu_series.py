@@ -350,3 +350,28 @@ def test_series_and_gram_empty_and_single_mode_edges():
     f1 = zb.series_eval(modes, np.arange(M, dtype=float), rho1, theta1)
     B1 = orc.basis_2d([(md.n, md.m) for md in modes], rho1, theta1)
     assert np.abs(f1 - B1 @ np.arange(M)).max() <= 1e-12 * np.abs(B1).sum() * M
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_series_random_requests_against_oracle(seed):
+    """Seeded random requests through every series engine the dispatcher picks:
+    random mode lists (duplicates, sign flips, sparse alpha), 1..10 vectors,
+    derivative order 0..3, 2-D or radial, point counts that are not tile
+    multiples; every entry against B @ C of the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    nmax = int(rng.integers(1, 40))
+    pool = [(n, m) for n in range(nmax + 1) for m in range(-n, n + 1, 2)]
+    M = int(rng.integers(1, min(len(pool), 120) + 1))
+    pairs_ = [pool[i] for i in rng.integers(0, len(pool), size=M)]
+    modes = zb.as_mode_set(pairs_)
+    V = int(rng.integers(1, 11))
+    k = int(rng.integers(0, 4))
+    P = int(rng.integers(1, 2500))
+    rho, theta = disc(P, seed)
+    two_d = bool(rng.integers(0, 2))
+    C = rng.standard_normal((M, V))
+    f = zb.series_eval(modes, C, rho, theta if two_d else None, k)
+    B = orc.basis_2d(pairs_, rho, theta, k) if two_d else orc.radial_batch(pairs_, rho, k)
+    scale = np.abs(B) @ np.abs(C)
+    err = np.abs(f.reshape(P, V) - B @ C)
+    assert (err <= 1e-12 * scale + 1e-300).all(), (seed, M, V, k, P, two_d, float(err.max()))
