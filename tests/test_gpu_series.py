@@ -375,3 +375,31 @@ def test_series_random_requests_against_oracle(seed):
     scale = np.abs(B) @ np.abs(C)
     err = np.abs(f.reshape(P, V) - B @ C)
     assert (err <= 1e-12 * scale + 1e-300).all(), (seed, M, V, k, P, two_d, float(err.max()))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_gram_random_requests_against_numpy(monkeypatch, seed):
+    """Seeded random normal-equation requests: random mode lists (so M + 1 hits
+    every residue mod the 64-column block), 2-D or radial, point counts that
+    are not multiples of the 16-point step, one or several panels; G and B^T y
+    against numpy on the oracle basis, G exactly symmetric."""
+    rng = np.random.default_rng(2000 + seed)
+    nmax = int(rng.integers(1, 30))
+    pool = [(n, m) for n in range(nmax + 1) for m in range(-n, n + 1, 2)]
+    M = int(rng.integers(1, min(len(pool), 200) + 1))
+    pairs_ = [pool[i] for i in rng.integers(0, len(pool), size=M)]
+    modes = zb.as_mode_set(pairs_)
+    P = int(rng.integers(1, 6000))
+    rho, theta = disc(P, 50 + seed)
+    two_d = bool(rng.integers(0, 2))
+    y = rng.standard_normal(P)
+    if seed % 2:
+        monkeypatch.setenv("ZK_GRAM_PANEL_MB", "1")  # several panels
+    G, r = zb.gram(modes, rho, theta if two_d else None, y)
+    G = np.asarray(G.cpu() if hasattr(G, "cpu") else G)
+    r = np.asarray(r.cpu() if hasattr(r, "cpu") else r)
+    B = orc.basis_2d(pairs_, rho, theta) if two_d else orc.radial_batch(pairs_, rho, 0)
+    gs = np.abs(B).T @ np.abs(B)
+    assert (np.abs(G - B.T @ B) <= 1e-12 * gs + 1e-300).all(), (seed, M, P, two_d)
+    assert np.array_equal(G, G.T)
+    assert (np.abs(r - B.T @ y) <= 1e-12 * (np.abs(B).T @ np.abs(y)) + 1e-300).all()
