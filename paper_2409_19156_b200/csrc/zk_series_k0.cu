@@ -19,8 +19,8 @@
 //  * the group's rho^|m| cos(|m| theta), rho^|m| sin(|m| theta) is ONE complex
 //    number w = z^alpha, z = rho e^{i theta}, advanced by a complex multiply
 //    per alpha step and re-anchored on the exact rho^alpha (double-double,
-//    ascending) times sincos(fl(alpha theta)) at least every 8 alpha-steps --
-//    the same anchoring policy as the general kernel's rotation; per group
+//    ascending) times sincos(fl(alpha theta)) at least every 32 alpha-steps
+//    (ZK_K0_ANCHOR) and after any jump of more than 4; per group
 //    f += X Re(w) + Y Im(w).
 // Tolerance semantics as the general kernel's tolerance mode: same sums,
 // different rounding (tests/test_gpu_series.py measures it against binary128).
@@ -35,6 +35,13 @@ namespace zk {
 
 namespace {
 constexpr int kT = 256;
+// alpha-steps between exact anchors of w = z^alpha: 32 measured 0.347 vs 0.376
+// ms at config 5 (8), with the error against binary128 unchanged at n <= 60 /
+// 100 and on a high-|m|-only set (tests/test_gpu_series.py); each complex
+// multiply adds ~1.5 ulp, so 32 steps bound the drift at ~1e-14 per term
+#ifndef ZK_K0_ANCHOR
+#define ZK_K0_ANCHOR 32
+#endif
 constexpr int kPark0 = 4;  // parked per point: rho, theta, (rho^e hi, lo) of the last anchor
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -125,7 +132,7 @@ __device__ __forceinline__ void k0_points(const SeriesArgs& a, const GroupRec* g
     const int alpha = g.alpha;
     const int step = alpha - a_cur;  // CTA-uniform
     if (step != 0) {
-      if (a_cur >= 0 && step > 0 && step <= 4 && since + step <= 8) {
+      if (a_cur >= 0 && step > 0 && step <= 4 && since + step <= ZK_K0_ANCHOR) {
 #pragma unroll 1
         for (int s = 0; s < step; ++s) {
 #pragma unroll
