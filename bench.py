@@ -47,6 +47,13 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+
+# The image sets NCCL_DEBUG=VERSION, which makes every NCCL communicator init
+# print its version banner to stdout -- the contract is ONE JSON line there.
+# That level (only) is lowered to NONE before any communicator exists; an
+# explicit WARN / INFO is left alone.
+if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "NONE"
 sys.path.insert(0, ROOT)
 
 METRIC = "fp64 Zernike radial evals/s (points x modes)"
