@@ -532,6 +532,51 @@ def test_single_order_cta_sizes_agree_bitwise(tmp_path):
         assert within_tolerance(outs[0][i][:50], ref)
 
 
+@pytest.mark.parametrize("env", [
+    {"ZK_STAGED": "0"},                              # round 1's land-in-place + fill pipeline
+    {"ZK_STAGED": "0", "ZK_BOUNCE": "0"},            # ... without pinned bounce buffers
+    {"ZK_UNIQUE_D2H": "0"},                          # every column over PCIe
+    {"ZK_RING_SLOTS": "2", "ZK_RING_MB": "1"},       # tiny staging ring
+    {"ZK_IMAGE_MB": "64"},                           # several point chunks of the device image
+    {"ZK_HOST_THREADS": "1"},                        # copy-out on the calling thread only
+])
+def test_host_output_paths_bitwise(monkeypatch, env):
+    """Every host-output path (read per call) writes the bits of the default
+    staged path, for pageable (fresh numpy) and page-locked destinations,
+    radial with repeated keys and 2-D, all orders."""
+    modes = zb.full_mode_set(40)
+    n = np.array([md.n for md in modes], np.int32)
+    m = np.array([md.m for md in modes], np.int32)
+    grid = np.random.default_rng(31).uniform(size=30001)
+    th = np.random.default_rng(32).uniform(-3, 3, size=30001)
+    base = zb.evaluate_batch_all_orders(zb.BatchRequest(modes=modes, grid=grid, deriv_order=2))
+    base2d = zb.zernike_basis(grid, th, n, m)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got = zb.evaluate_batch_all_orders(zb.BatchRequest(modes=modes, grid=grid, deriv_order=2))
+    got2d = zb.zernike_basis(grid, th, n, m)
+    for a, b in zip(base, got):
+        assert np.array_equal(a.values, b.values)
+    assert np.array_equal(base2d, got2d)
+    # a page-locked destination through the C ABI
+    import ctypes
+    ctx = zb._lib.context()
+    plan = zb._lib.plan_for(ctx, n, m)
+    P, M = grid.size, n.size
+    hbuf = ctypes.c_void_p()
+    zb._lib.check(zb._lib.lib.zk_host_alloc(8 * P * M, ctypes.byref(hbuf)), "zk_host_alloc")
+    try:
+        zb._lib.check(zb._lib.lib.zk_radial_eval(
+            ctx.handle, plan.handle, grid.ctypes.data, P, 0, 0, hbuf.value, P, 0,
+            zb._lib.ZK_HOST_INPUT | zb._lib.ZK_HOST_OUTPUT), "zk_radial_eval")
+        view = np.ctypeslib.as_array(ctypes.cast(hbuf.value, ctypes.POINTER(ctypes.c_double)),
+                                     shape=(M, P))
+        assert np.array_equal(view.T, base[0].values)
+        del view
+    finally:
+        zb._lib.lib.zk_host_free(hbuf)
+
+
 def test_parallel_shards_over_devices_bitwise(monkeypatch):
     """parallel=True splits the points across devices (here: two shards on
     the one available GPU via ZK_DEVICES=0,0); every shard writes its rows of

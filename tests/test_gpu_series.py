@@ -141,6 +141,8 @@ ENGINES = {  # single-vector k = 0 series engines (environment switches read per
     "staged_scaled": {"ZK_SERIES_K0": "0"},
     "staged_unscaled": {"ZK_SERIES_K0": "0", "ZK_SERIES_SCALED": "0"},
     "exact": {"ZK_SERIES_EXACT": "1"},
+    "staged_resident": {"ZK_SERIES_K0": "0", "ZK_SERIES_RESIDENT": "1"},
+    "staged_vec2": {"ZK_SERIES_K0": "0", "ZK_SERIES_VEC3": "0"},
 }
 
 
