@@ -432,3 +432,29 @@ def test_series_high_alpha_terms_accuracy_vs_binary128(monkeypatch):
         errs[mode] = float((np.abs(f - ref) / scale).max())
     print(f"high-alpha series error {errs['0']:.3e} (exact engine {errs['1']:.3e}) of sum|B||c|")
     assert errs["0"] <= 2 * errs["1"] + 1e-15
+
+
+def test_gram_panel_geometries_bitwise(monkeypatch):
+    """The Gram is bitwise independent of its panel geometry switches read per
+    call: one panel, several double-buffered panels (K2 of panel i+1 overlapping
+    the SYRK of panel i), and several panels without the overlap."""
+    modes = zb.full_mode_set(20)
+    rho, theta = disc(40_000, 71)
+    y = np.random.default_rng(72).standard_normal(40_000)
+    outs = []
+    for env in ({}, {"ZK_GRAM_PANEL_MB": "1"}, {"ZK_GRAM_PANEL_MB": "1", "ZK_GRAM_OVERLAP": "0"}):
+        for k in ("ZK_GRAM_PANEL_MB", "ZK_GRAM_OVERLAP"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        G, r = zb.gram(modes, rho, theta, y)
+        outs.append((np.asarray(G.cpu() if hasattr(G, "cpu") else G),
+                     np.asarray(r.cpu() if hasattr(r, "cpu") else r)))
+    # the panel split changes the summation order across panels, so one panel
+    # vs several is tolerance-equal; the overlap switch alone is bitwise
+    assert np.array_equal(outs[1][0], outs[2][0]) and np.array_equal(outs[1][1], outs[2][1])
+    B = orc.basis_2d([(md.n, md.m) for md in modes], rho, theta)
+    gs = np.abs(B).T @ np.abs(B)
+    for G, r in outs:
+        assert (np.abs(G - B.T @ B) <= 1e-12 * gs).all()
+        assert (np.abs(r - B.T @ y) <= 1e-12 * (np.abs(B).T @ np.abs(y))).all()
