@@ -796,3 +796,53 @@ def test_recycled_result_buffers_are_page_locked(monkeypatch):
     gc.collect()
     pool.clear()
     assert not pool.pinned
+
+
+def test_device_calls_are_cuda_graph_capturable():
+    """The device-resident C-ABI calls (radial, 2-D, series) can be captured into
+    a CUDA graph on the caller's stream (no host synchronisation or allocation
+    inside a warm call) and replay bitwise (tools/graph_capture_check.py times
+    it at config-2 size)."""
+    import torch
+    modes = zb.full_mode_set(30)
+    n = np.array([md.n for md in modes], np.int32)
+    m = np.array([md.m for md in modes], np.int32)
+    M, P = n.size, 5000
+    ctx = zb._lib.context(0)
+    plan = zb._lib.plan_for(ctx, n, m)
+    rho = torch.from_numpy(np.random.default_rng(3).uniform(size=P)).cuda()
+    th = torch.from_numpy(np.random.default_rng(4).uniform(-3, 3, size=P)).cuda()
+    coef = torch.from_numpy(np.random.default_rng(5).standard_normal(M)).cuda()
+    out = torch.empty(M * P, dtype=torch.float64, device="cuda")
+    out2 = torch.empty(M * P, dtype=torch.float64, device="cuda")
+    f = torch.empty(P, dtype=torch.float64, device="cuda")
+    A = zb._lib.ZK_ASYNC
+
+    def calls():
+        zb._lib.check(zb._lib.lib.zk_radial_eval(ctx.handle, plan.handle, rho.data_ptr(), P, 2, 1,
+                                                 out.data_ptr(), P, M * P, A), "radial")
+        zb._lib.check(zb._lib.lib.zk_zernike_eval(ctx.handle, plan.handle, rho.data_ptr(),
+                                                  th.data_ptr(), P, 0, 0, out2.data_ptr(), P, 0,
+                                                  A), "2d")
+        zb._lib.check(zb._lib.lib.zk_series_eval(ctx.handle, plan.handle, rho.data_ptr(),
+                                                 th.data_ptr(), P, 0, coef.data_ptr(), 1, M,
+                                                 f.data_ptr(), P, A), "series")
+
+    out = torch.empty(3 * M * P, dtype=torch.float64, device="cuda")  # orders 0..2
+    s = torch.cuda.Stream()
+    ctx.set_stream(s.cuda_stream)
+    try:
+        with torch.cuda.stream(s):
+            calls()
+        torch.cuda.synchronize()
+        eager = (out.clone(), out2.clone(), f.clone())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            calls()
+        out.zero_(), out2.zero_(), f.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for a, b in zip(eager, (out, out2, f)):
+            assert torch.equal(a, b)
+    finally:
+        ctx.set_stream(None)
