@@ -458,3 +458,51 @@ def test_gram_panel_geometries_bitwise(monkeypatch):
     for G, r in outs:
         assert (np.abs(G - B.T @ B) <= 1e-12 * gs).all()
         assert (np.abs(r - B.T @ y) <= 1e-12 * (np.abs(B).T @ np.abs(y))).all()
+
+
+@pytest.mark.parametrize("panel_mb", [None, "1"])
+def test_gram_accumulate_is_cuda_graph_capturable(monkeypatch, panel_mb):
+    """zk_gram_accumulate on device buffers captures into a CUDA graph on the
+    caller's stream -- one panel, or several double-buffered panels whose K2
+    runs on the library's second stream (joined through events) -- and the
+    replay is bitwise the eager call."""
+    import torch
+    if panel_mb:
+        monkeypatch.setenv("ZK_GRAM_PANEL_MB", panel_mb)
+    modes = zb.full_mode_set(30)
+    n = np.array([md.n for md in modes], np.int32)
+    m = np.array([md.m for md in modes], np.int32)
+    M, P = n.size, 20_000
+    ctx = zb._lib.context(0)
+    plan = zb._lib.plan_for(ctx, n, m)
+    rng = np.random.default_rng(9)
+    rho = torch.from_numpy(np.sqrt(rng.uniform(size=P))).cuda()
+    th = torch.from_numpy(rng.uniform(-3, 3, size=P)).cuda()
+    y = torch.from_numpy(rng.standard_normal(P)).cuda()
+    G = torch.zeros((M, M), dtype=torch.float64, device="cuda")
+    r = torch.zeros(M, dtype=torch.float64, device="cuda")
+
+    def call():
+        G.zero_()
+        r.zero_()
+        zb._lib.check(zb._lib.lib.zk_gram_accumulate(ctx.handle, plan.handle, rho.data_ptr(),
+                                                     th.data_ptr(), P, y.data_ptr(), G.data_ptr(),
+                                                     r.data_ptr(), zb._lib.ZK_ASYNC), "gram")
+
+    s = torch.cuda.Stream()
+    ctx.set_stream(s.cuda_stream)
+    try:
+        with torch.cuda.stream(s):
+            call()
+        torch.cuda.synchronize()
+        eager = (G.clone(), r.clone())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            call()
+        G.fill_(7.0)
+        r.fill_(7.0)
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(eager[0], G) and torch.equal(eager[1], r)
+    finally:
+        ctx.set_stream(None)
