@@ -506,3 +506,27 @@ def test_gram_accumulate_is_cuda_graph_capturable(monkeypatch, panel_mb):
         assert torch.equal(eager[0], G) and torch.equal(eager[1], r)
     finally:
         ctx.set_stream(None)
+
+
+def test_concurrent_mixed_entry_points_share_a_context():
+    """Host threads mixing the series, the Gram and the 2-D basis on one device
+    context (one call at a time per context; the staged host paths share its
+    scratch and ring) get the serial results bitwise."""
+    from concurrent.futures import ThreadPoolExecutor
+    modes = zb.full_mode_set(25)
+    n = np.array([md.n for md in modes], np.int32)
+    m = np.array([md.m for md in modes], np.int32)
+    rho, theta = disc(20_000, 81)
+    c = np.random.default_rng(82).standard_normal(len(modes))
+    y = np.random.default_rng(83).standard_normal(20_000)
+    def gram_g():
+        G = zb.gram(modes, rho, theta, y)[0]
+        return np.asarray(G.cpu() if hasattr(G, "cpu") else G)
+
+    jobs = [lambda: zb.series_eval(modes, c, rho, theta), gram_g,
+            lambda: zb.zernike_basis(rho, theta, n, m)]
+    want = [j() for j in jobs]
+    with ThreadPoolExecutor(6) as pool:
+        got = list(pool.map(lambda i: jobs[i % 3](), range(18)))
+    for i, g in enumerate(got):
+        assert np.array_equal(g, want[i % 3]), i
