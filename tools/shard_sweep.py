@@ -48,3 +48,50 @@ for world in (1, 2, 4, 8):
     print(json.dumps({"gpus": world, "shard_points": P, "shard_ms": ms, "shard_GBps": gbs,
                       "ideal_aggregate_evals_per_s": 100_000 * M / (ms * 1e-3)}), flush=True)
     del out
+
+# config 5's fit per rank: the series (K3) and the normal equations (K4) on the
+# rank's 1e6/N disc points; K5 (one allreduce of 14.3 MB) and K6 (the 1891 x
+# 1891 Cholesky) are per-step constants not timed here
+modes5 = zb.full_mode_set(60)
+n5, m5 = zb.modes.mode_arrays(modes5)
+M5 = len(modes5)
+plan5 = _lib.plan_for(ctx, n5, m5)
+rng = np.random.default_rng(0)
+rho5 = np.sqrt(rng.uniform(size=1_000_000))
+th5 = 2 * np.pi * rng.uniform(size=1_000_000)
+coef5 = torch.from_numpy(rng.standard_normal(M5)).cuda()
+for world in (1, 2, 4, 8):
+    lo, hi = zb.shard_range(1_000_000, world, 0)
+    P = hi - lo
+    rho = torch.from_numpy(np.ascontiguousarray(rho5[lo:hi])).cuda()
+    th = torch.from_numpy(np.ascontiguousarray(th5[lo:hi])).cuda()
+    y = torch.empty(P, dtype=torch.float64, device="cuda")
+    G = torch.zeros((M5, M5), dtype=torch.float64, device="cuda")
+    r = torch.zeros(M5, dtype=torch.float64, device="cuda")
+
+    def k3():
+        _lib.check(_lib.lib.zk_series_eval(ctx.handle, plan5.handle, rho.data_ptr(), th.data_ptr(), P,
+                                           0, coef5.data_ptr(), 1, M5, y.data_ptr(), P,
+                                           _lib.ZK_ASYNC), "series")
+
+    def k4():
+        _lib.check(_lib.lib.zk_gram_accumulate(ctx.handle, plan5.handle, rho.data_ptr(),
+                                               th.data_ptr(), P, y.data_ptr(), G.data_ptr(),
+                                               r.data_ptr(), _lib.ZK_ASYNC), "gram")
+
+    res = {}
+    for name, fn, reps in (("series_ms", k3, 20), ("gram_ms", k4, 3)):
+        with torch.cuda.stream(stream):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(reps):
+                fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res[name] = e0.elapsed_time(e1) / reps
+    print(json.dumps({"c5fit_gpus": world, "shard_points": P, **res,
+                      "gram_alg_tflops": P * (M5 + 1) * (M5 + 2) / (res["gram_ms"] * 1e-3) / 1e12}),
+          flush=True)
