@@ -530,3 +530,19 @@ def test_concurrent_mixed_entry_points_share_a_context():
         got = list(pool.map(lambda i: jobs[i % 3](), range(18)))
     for i, g in enumerate(got):
         assert np.array_equal(g, want[i % 3]), i
+
+
+def test_solve_normal_rejects_an_indefinite_normal_matrix():
+    """K6 raises torch.linalg.LinAlgError (as torch.linalg.cholesky would) when
+    the matrix is not positive definite, and a duplicated mode (two equal
+    columns of B: singular G) solves once regularised."""
+    import torch
+    modes = zb.as_mode_set([(2, 0), (2, 0), (4, 2)])
+    rho, theta = disc(500, 91)
+    y = np.random.default_rng(92).standard_normal(500)
+    G, r = zb.gram(modes, rho, theta, y)
+    G = torch.as_tensor(G, device="cuda")
+    with pytest.raises(torch.linalg.LinAlgError):
+        zb.solve_normal(-G, r)
+    x = zb.solve_normal(G, r, ridge=1e-9 * float(G.diagonal().max()))
+    assert torch.isfinite(x).all()
