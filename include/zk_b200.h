@@ -195,6 +195,21 @@ int zk_comm_info(const zk_comm* comm, int* nranks, int* rank);
 int zk_comm_destroy(zk_comm* comm);
 int zk_gram_allreduce_comm(zk_comm* comm, double* G, double* Bty, int64_t M, uint32_t flags);
 
+/* ---- fp64-emulated Gram building blocks (opt-in; gram_emulated.py) -------
+ * Replaces nothing in the reference (the normal equations are config 5's
+ * addition). The fp64 panel [B y] (column j at B + j*ld, P points) is split
+ * into S int8 slices per column after scaling by 2^-e_j (e_j: max|b_j| <
+ * 2^e_j); slice products run as exact int32 tensor-core GEMMs elsewhere and
+ * are recombined here in fp64: G[i + j*ldg] += 2^(e_i+e_j-shift) (C[i][j] +
+ * sym * C[j][i]), C n-major with leading dimension ldc. All pointers are
+ * device pointers; `stream` is a cudaStream_t (NULL: the legacy stream). */
+int zk_emul_colexp(const double* B, int64_t ld, int64_t P, int64_t M, int32_t* e, void* stream);
+int zk_emul_slices(const double* B, int64_t ld, int64_t P, int64_t M, const int32_t* e, int S,
+                   int8_t* out /* nch x S x Mpad x kc: chunk-major, point-fastest */,
+                   int64_t kc, int64_t nch, int64_t Mpad, void* stream);
+int zk_emul_accumulate(const int32_t* C, int64_t ldc, int64_t M, const int32_t* e, int shift,
+                       int sym, double* G, int64_t ldg, void* stream);
+
 /* ---- jacobi_chain export ------------------------------------------------
  * Rows P_0..P_{j_max} of the Jacobi chain (alpha, beta >= 0) at x[N]:
  * row j at out[j*ldo + p], ldo >= N (zk/evaluate.py:36-76 jacobi_chain, the

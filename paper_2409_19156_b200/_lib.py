@@ -88,6 +88,11 @@ SIGNATURES = {
     "zk_comm_info": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int)]),
     "zk_comm_destroy": (c_int, [c_void_p]),
     "zk_gram_allreduce_comm": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_uint32]),
+    "zk_emul_colexp": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
+    "zk_emul_slices": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int, c_void_p,
+                               c_int64, c_int64, c_int64, c_void_p]),
+    "zk_emul_accumulate": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int, c_int,
+                                   c_void_p, c_int64, c_void_p]),
     "zk_host_alloc": (c_int, [c_int64, POINTER(c_void_p)]),
     "zk_host_free": (c_int, [c_void_p]),
 }

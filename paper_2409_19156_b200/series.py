@@ -17,6 +17,8 @@ tensors stay on the device.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -241,7 +243,14 @@ def _gram_device_nm(n, m, rho, theta, y, G, Bty):
     theta = theta.contiguous() if theta is not None else None
     y = y.contiguous() if y is not None else None
     P = rho.numel()
-    if P and M:
+    if P and M and os.environ.get("ZK_GRAM_EMULATED", "0") == "1":
+        # opt-in: int8 slice products on tcgen05 (gram_emulated.py)
+        from .gram_emulated import gram_emulated_nm
+        Ge, be = gram_emulated_nm(n, m, rho, theta, y)
+        G += Ge
+        if Bty is not None and be is not None:
+            Bty += be
+    elif P and M:
         ctx = _torch_ctx(rho, None)
         plan = _lib.plan_for(ctx, n, m)
         _lib.check(_lib.lib.zk_gram_accumulate(
