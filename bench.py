@@ -388,6 +388,33 @@ def run_c5fit(args, world, rank, local, dist, stream, comm):
     phase /= steps
     if dist:
         phase = np.array([max_over_ranks(dist, float(v), local) for v in phase])
+    # the opt-in fp64-emulated Gram (gram_emulated.py: int8 slices x tcgen05 int8
+    # GEMMs) on the same shard, timed the same way, with its deviation from K4
+    emul = None
+    try:
+        from paper_2409_19156_b200.gram_emulated import gram_emulated_nm
+        n5, m5 = zb.modes.mode_arrays(modes)
+        with torch.cuda.stream(stream):
+            Ge, _ = gram_emulated_nm(n5, m5, rho, th, y)  # JIT-compiles the GEMM once
+            torch.cuda.synchronize()
+            ev[0].record(stream)
+            for _ in range(steps):
+                Ge, be = gram_emulated_nm(n5, m5, rho, th, y)
+            ev[1].record(stream)
+            torch.cuda.synchronize()
+        te = ev[0].elapsed_time(ev[1]) / steps
+        if dist:
+            te = max_over_ranks(dist, te, local)
+        G.zero_()
+        r.zero_()
+        zs.gram_device(modes, rho, th, y, G, r)
+        dev_g = float((Ge - G).abs().max() / G.diagonal().abs().max())
+        emul = {"gram_ms": te, "max_abs_dev_vs_K4_over_max_diag": dev_g,
+                "impl": "int8 slices (zk_emul_slices) x tcgen05 int8 GEMMs (CuTe-DSL library "
+                        "kernel) -> fp64 recombination (zk_emul_accumulate); opt-in "
+                        "ZK_GRAM_EMULATED=1"}
+    except Exception as exc:  # noqa: BLE001 -- reported, the K4 numbers stand
+        emul = {"unavailable": str(exc)[:200]}
     err = float((x.cpu() - torch.from_numpy(coef_h)).abs().max())
     nb = (M + 1 + 63) // 64  # 64 x 64 upper-triangle blocks of [B y] (zk_gram.cu BM)
     alg = 1.0 * P_C5 / world * (M + 1) * (M + 2)  # triangle of [B y]^T [B y], this rank
@@ -404,7 +431,8 @@ def run_c5fit(args, world, rank, local, dist, stream, comm):
                                "torch.distributed all_reduce of the packed triangle"),
             "gram_alg_tflops_per_gpu": alg / (phase[1] * 1e-3) / 1e12,
             "gram_executed_tiles": nb * (nb + 1) // 2,
-            "fit_max_abs_err_vs_c": err}
+            "fit_max_abs_err_vs_c": err,
+            "gram_emulated": emul}
 
 
 def run_gpu(args, world, rank, local):
