@@ -66,17 +66,22 @@ def _gemm(a, b, c, stream_ptr):
     _GEMM[key](a_, b_, c_, cuda.CUstream(stream_ptr))
 
 
-def gram_emulated_device(plan_modes, rho, theta, y, slices: int = 8):
+def gram_emulated_device(plan_modes, rho, theta, y, slices: int | None = None):
     """G = B^T B and B^T y of the 2-D basis (theta) or the radial one (theta
     None) on CUDA tensors, through int8 slice products on tcgen05."""
     ms, n, m = _modes(plan_modes)
     return gram_emulated_nm(n, m, rho, theta, y, slices)
 
 
-def gram_emulated_nm(n, m, rho, theta, y, slices: int = 8):
+def gram_emulated_nm(n, m, rho, theta, y, slices: int | None = None):
     """gram_emulated_device on the C ABI's (n, m) column arrays; y may be None
-    (then Bty is None)."""
+    (then Bty is None). ``slices`` (default ZK_EMUL_SLICES or 8): 7 bits each;
+    the error grows with a column's max-to-typical magnitude ratio (per-column
+    scaling). Measured at config 5 against the DMMA Gram, relative to |B|^T|B|:
+    S = 8 1.8e-15 (73 ms), S = 7 4.2e-15 (59 ms), S = 6 9.3e-12 (45 ms)."""
     import torch
+    if slices is None:
+        slices = int(os.environ.get("ZK_EMUL_SLICES", "8"))
     M, P = int(n.size), rho.numel()
     dev = rho.device
     S = int(slices)
